@@ -1,0 +1,149 @@
+/*
+ * binarsort_b200.h -- C ABI of the B200-native Binar Sort hot path.
+ *
+ * The reference (arxiv 0811.3448, package `binarsort`) routes a 1-D word
+ * array to its numba kernel module through `KeyCodec.words_view`
+ * (/root/reference/pkg/src/binarsort/keys.py:140-149,175-178) and then calls
+ *
+ *     kernels.sort_words(words, 0, n-1, 0, width, False, 0, 0, False, counters, 1)
+ *
+ * (core.py:213-219, kernels.py:88-126).  The entry points below replace that
+ * kernel-module ABI (kernels.py:52-172) for device-resident buffers.  All
+ * pointers named `keys`, `vals`, `ws`, `counters` are DEVICE pointers; `stream`
+ * is a cudaStream_t (NULL = legacy default stream).  No call allocates device
+ * memory, keeps global mutable state, or synchronises the stream unless it
+ * says so; calls on distinct streams with distinct buffers are independent.
+ *
+ * Status codes map onto the reference's exception types in the Python shim:
+ *   BS_ERR_VALUE  -> ValueError      (bad configuration, keys.py:164-165 etc.)
+ *   BS_ERR_ASSERT -> AssertionError  (contract violation, core.py:102-105)
+ *   BS_ERR_CUDA / BS_ERR_WORKSPACE / BS_ERR_INTERNAL -> RuntimeError
+ * bs_last_error() returns a thread-local message for the last failing call.
+ */
+#ifndef BINARSORT_B200_H
+#define BINARSORT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BS_OK 0
+#define BS_ERR_VALUE 1
+#define BS_ERR_ASSERT 2
+#define BS_ERR_CUDA 3
+#define BS_ERR_WORKSPACE 4
+#define BS_ERR_INTERNAL 5
+
+/* key_kind: the codec's order-preserving word transform (keys.py:51-93). */
+#define BS_KEY_UNSIGNED 0 /* UnsignedCodec(width): identity, low `width` bits  */
+#define BS_KEY_SIGNED 1   /* SignedCodec(width): flip bit width-1 (two's compl.) */
+#define BS_KEY_FLOAT 2    /* Float64Codec: IEEE-754 total-order transform       */
+
+/* Library version (major*10000 + minor*100 + patch). */
+int bs_version(void);
+
+/* Thread-local message for the last non-BS_OK return on this thread. */
+const char *bs_last_error(void);
+
+/*
+ * Workspace bytes bs_sort needs for n elements (replaces nothing in the
+ * reference: the numba kernel is in-place; the GPU MSD ping-pongs through a
+ * second buffer of n*(key_bytes+val_bytes) plus O(n/1024) bucket metadata).
+ * key_bytes in {4, 8}; val_bytes in {0, 4, 8}.
+ */
+size_t bs_workspace_bytes(uint64_t n, int key_bytes, int val_bytes);
+
+/*
+ * Sort keys[0..n) (and vals[0..n) alongside, if vals != NULL) in place into
+ * nondecreasing codec order.  Replaces kernels.sort_words(arr, lower, upper,
+ * pos, width, False, 0, 0, False, counters, depth) (kernels.py:88-126) for the
+ * sub-range arr[lower..upper]: pass keys = arr + lower, n = upper-lower+1,
+ * start_pos = pos.  The sort key of a word is its low `width` bits read from
+ * bit (width-1-start_pos) down to bit 0 (kernels.py:63,69), after the
+ * key_kind transform.
+ *
+ * Keys-only output is the unique nondecreasing sequence, hence bit-exact with
+ * the reference.  With vals the sort is STABLE (ties keep input order), which
+ * is exactly the order the reference produces on packed (key<<32|index) words
+ * (SURVEY §8c).  `counters`, if non-NULL, is a device int64[4] that receives
+ * the reference Metrics {bit_extractions, swaps, recursive_calls, max_depth}
+ * of the baseline recursive sort started at `depth` (closed form over the
+ * sorted output); it is written asynchronously.
+ */
+int bs_sort(void *keys, void *vals, uint64_t n, int key_bytes, int val_bytes,
+            int width, int start_pos, int key_kind, void *ws, size_t ws_bytes,
+            void *stream, int64_t *counters, int64_t depth);
+
+/*
+ * Reference Metrics of kernels.sort_words over an ALREADY SORTED device array
+ * (the K6 closed form).  Adds into the device int64[4]
+ * `counters` with Metrics.merge semantics (core.py:60-77): counts add,
+ * max_depth takes the max.  ws must hold bs_metrics_workspace_bytes(n).
+ */
+size_t bs_metrics_workspace_bytes(uint64_t n);
+int bs_metrics(const void *sorted_keys, uint64_t n, int key_bytes, int width,
+               int start_pos, int key_kind, int64_t depth, void *ws,
+               size_t ws_bytes, void *stream, int64_t *counters);
+
+/*
+ * One reference partition pass (kernels.partition_words, kernels.py:56-77) on
+ * keys[0..n) at bit `pos`, reproducing the reference's exact (unstable)
+ * two-cursor permutation via its closed form; vals (may be
+ * NULL) receive the same permutation.  The bit is read from the raw word as
+ * (x << pos) & (1 << (width-1)) (kernels.py:63,69).  Writes the split index
+ * (relative to keys) to *split_dev (device int64) and adds n extractions and
+ * the swap count into counters (device int64[4], may be NULL).  ws must hold
+ * bs_partition_workspace_bytes(n, key_bytes, val_bytes).
+ */
+size_t bs_partition_workspace_bytes(uint64_t n, int key_bytes, int val_bytes);
+int bs_partition_words(void *keys, void *vals, uint64_t n, int key_bytes,
+                       int val_bytes, int width, int pos, void *ws,
+                       size_t ws_bytes, void *stream, int64_t *split_dev,
+                       int64_t *counters);
+
+/*
+ * kernels.range_sorted_words (kernels.py:80-85): writes 1 to *flag_dev
+ * (device int32) iff keys[0..n) is nondecreasing as unsigned words.
+ */
+int bs_range_sorted(const void *keys, uint64_t n, int key_bytes, void *stream,
+                    int32_t *flag_dev);
+
+/* ---------------------------------------------------------------------------
+ * Multi-GPU front end (replaces variants.sort_parallel's serial top-bit
+ * pre-partition + thread pool, variants.py:124-229).  The collective itself
+ * (count exchange + all-to-all-v) is issued by the host over NCCL; these are
+ * the per-rank device steps around it.
+ * ------------------------------------------------------------------------- */
+
+/*
+ * Stable partition of keys[0..n) (+vals) into 2*R-1 destination classes given
+ * R-1 nondecreasing splitter words (device, already key_kind-encoded and
+ * normalised to the top of the word): class 2j = keys strictly between
+ * splitter j-1 and splitter j, class 2j+1 = keys equal to splitter j.  The
+ * result goes to out_keys/out_vals (device, n elements) and the 2R-1 class
+ * counts to class_counts (device uint64).  ws: bs_split_workspace_bytes.
+ */
+size_t bs_split_workspace_bytes(uint64_t n, int key_bytes, int val_bytes, int nranks);
+int bs_split_by_splitters(const void *keys, const void *vals, uint64_t n,
+                          int key_bytes, int val_bytes, int width,
+                          int key_kind, const void *splitters, int nranks,
+                          void *out_keys, void *out_vals, uint64_t *class_counts,
+                          void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * Gather `count` uniformly strided samples of the encoded, normalised sort key
+ * (device, key_bytes words) from keys[0..n): sample i is element
+ * floor((2i+1)*n/(2*count)).
+ */
+int bs_sample_keys(const void *keys, uint64_t n, int key_bytes, int width,
+                   int key_kind, uint64_t count, void *out_samples,
+                   void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BINARSORT_B200_H */

@@ -1,0 +1,116 @@
+"""Loader for the C-ABI library ``libbinarsort_b200.so`` (include/binarsort_b200.h).
+
+The shared library is built in-tree by :func:`build` (``nvcc -gencode
+arch=compute_100a,code=sm_100a``).  There is no CPU fallback: if the library
+is missing or no CUDA device is present, every sort entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_ROOT = os.path.dirname(_HERE)
+SO_PATH = os.path.join(_HERE, "libbinarsort_b200.so")
+_CSRC = os.path.join(_HERE, "csrc")
+_SOURCES = ["binarsort_b200.cu"]
+_DEPS = ["binarsort_b200.cu", "common.cuh", "sort_impl.cuh", "metrics_impl.cuh", "misc_impl.cuh"]
+
+BS_OK, BS_ERR_VALUE, BS_ERR_ASSERT, BS_ERR_CUDA, BS_ERR_WORKSPACE, BS_ERR_INTERNAL = range(6)
+BS_KEY_UNSIGNED, BS_KEY_SIGNED, BS_KEY_FLOAT = 0, 1, 2
+
+NVCC_FLAGS = [
+    "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+    "-Xcompiler", "-fPIC", "-shared", "-Xcompiler", "-O3",
+]
+
+# every symbol include/binarsort_b200.h declares
+EXPORTS = (
+    "bs_version", "bs_last_error", "bs_workspace_bytes", "bs_sort",
+    "bs_metrics_workspace_bytes", "bs_metrics", "bs_partition_workspace_bytes",
+    "bs_partition_words", "bs_range_sorted", "bs_split_workspace_bytes",
+    "bs_split_by_splitters", "bs_sample_keys",
+)
+
+
+def _stale() -> bool:
+    if not os.path.exists(SO_PATH):
+        return True
+    so_m = os.path.getmtime(SO_PATH)
+    deps = [os.path.join(_CSRC, d) for d in _DEPS]
+    deps.append(os.path.join(_ROOT, "include", "binarsort_b200.h"))
+    return any(os.path.exists(d) and os.path.getmtime(d) > so_m for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile the CUDA library in-tree for sm_100a (no GPU needed)."""
+    if force or _stale():
+        nvcc = os.environ.get("NVCC", "nvcc")
+        if not os.path.isabs(nvcc) and os.path.exists("/usr/local/cuda/bin/nvcc"):
+            nvcc = "/usr/local/cuda/bin/nvcc"
+        tmp = SO_PATH + ".tmp"
+        cmd = [nvcc, *NVCC_FLAGS, "-o", tmp, *[os.path.join(_CSRC, s) for s in _SOURCES]]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+        os.replace(tmp, SO_PATH)
+    return SO_PATH
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib() -> ctypes.CDLL:
+    """The loaded library (raises if it was never built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(SO_PATH):
+            raise RuntimeError(
+                f"{SO_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+                " (there is no CPU fallback)")
+        L = ctypes.CDLL(SO_PATH)
+        vp, u64, i32, i64, sz = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int64, ctypes.c_size_t
+        L.bs_version.restype = i32
+        L.bs_last_error.restype = ctypes.c_char_p
+        L.bs_workspace_bytes.argtypes = [u64, i32, i32]
+        L.bs_workspace_bytes.restype = sz
+        L.bs_sort.argtypes = [vp, vp, u64, i32, i32, i32, i32, i32, vp, sz, vp, vp, i64]
+        L.bs_sort.restype = i32
+        L.bs_metrics_workspace_bytes.argtypes = [u64]
+        L.bs_metrics_workspace_bytes.restype = sz
+        L.bs_metrics.argtypes = [vp, u64, i32, i32, i32, i32, i64, vp, sz, vp, vp]
+        L.bs_metrics.restype = i32
+        L.bs_partition_workspace_bytes.argtypes = [u64, i32, i32]
+        L.bs_partition_workspace_bytes.restype = sz
+        L.bs_partition_words.argtypes = [vp, vp, u64, i32, i32, i32, i32, vp, sz, vp, vp, vp]
+        L.bs_partition_words.restype = i32
+        L.bs_range_sorted.argtypes = [vp, u64, i32, vp, vp]
+        L.bs_range_sorted.restype = i32
+        L.bs_split_workspace_bytes.argtypes = [u64, i32, i32, i32]
+        L.bs_split_workspace_bytes.restype = sz
+        L.bs_split_by_splitters.argtypes = [vp, vp, u64, i32, i32, i32, i32, vp, i32, vp, vp, vp, vp, sz, vp]
+        L.bs_split_by_splitters.restype = i32
+        L.bs_sample_keys.argtypes = [vp, u64, i32, i32, i32, u64, vp, vp]
+        L.bs_sample_keys.restype = i32
+        _lib = L
+        return L
+
+
+def check(rc: int) -> None:
+    """Map a C-ABI status to the reference's exception types."""
+    if rc == BS_OK:
+        return
+    msg = lib().bs_last_error().decode(errors="replace")
+    if rc == BS_ERR_VALUE:
+        raise ValueError(msg)
+    if rc == BS_ERR_ASSERT:
+        raise AssertionError(msg)
+    raise RuntimeError(f"binarsort_b200 error {rc}: {msg}")

@@ -1,0 +1,437 @@
+// binarsort_b200.cu -- host side of the C ABI declared in include/binarsort_b200.h.
+//
+// Launch sequence of bs_sort (all on the caller's stream, no host sync):
+//   memset(ctl) ; init ; for L in 0..ndig: { hist(L) ; plan(L) ; scatter(L) } ;
+//   local ; [metrics]
+// Levels that have no buckets exit immediately on the device.
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/binarsort_b200.h"
+#include "metrics_impl.cuh"
+#include "misc_impl.cuh"
+#include "sort_impl.cuh"
+
+namespace bs {
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+#define BS_CUDA(call)                                                                   \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(BS_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+
+static int num_sms() {
+  static int sms = 0;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  });
+  return sms;
+}
+
+// ----- tuning (per key width) ---------------------------------------------
+constexpr int SC_BLOCK = 512;
+constexpr int LC_BLOCK = 512;
+constexpr int LC_KPT = 16;
+constexpr int HI_BLOCK = 512;
+template <typename K> constexpr int sc_kpt() { return sizeof(K) == 4 ? 16 : 8; }
+
+struct Geometry {
+  uint64_t n;
+  int kb, vb;
+  uint32_t tile, local_max, group_min;
+  uint32_t maxb, maxtiles, maxtasks;
+  int ndig;
+};
+
+static Geometry geometry(uint64_t n, int kb, int vb, int width_eff) {
+  Geometry g{};
+  g.n = n;
+  g.kb = kb;
+  g.vb = vb;
+  g.tile = uint32_t(SC_BLOCK * (kb == 4 ? 16 : 8));
+  g.local_max = uint32_t(LC_BLOCK * LC_KPT);
+  g.group_min = g.local_max / 8;
+  g.ndig = (width_eff + 7) / 8;
+  const uint64_t maxb = n / (uint64_t(g.local_max) + 1) + 2;
+  const uint64_t maxtiles = n / g.tile + maxb + 2;
+  const uint64_t maxtasks = 3 * n / g.group_min + n / g.local_max + uint64_t(g.ndig + 2) * maxb + 1024;
+  g.maxb = uint32_t(maxb);
+  g.maxtiles = uint32_t(maxtiles);
+  g.maxtasks = uint32_t(maxtasks);
+  return g;
+}
+
+static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Layout {
+  size_t ctl, buckets[2], bhist[2], bor[2], band[2], tile_bucket[2], status, tasks, keys, vals, total;
+};
+
+static Layout layout(const Geometry &g) {
+  Layout l{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += align_up(bytes);
+    return o;
+  };
+  l.ctl = take(sizeof(Ctl));
+  for (int p = 0; p < 2; ++p) {
+    l.buckets[p] = take(sizeof(Bucket) * g.maxb);
+    l.bhist[p] = take(sizeof(uint32_t) * 256 * size_t(g.maxb));
+    l.bor[p] = take(sizeof(uint64_t) * g.maxb);
+    l.band[p] = take(sizeof(uint64_t) * g.maxb);
+    l.tile_bucket[p] = take(sizeof(uint32_t) * g.maxtiles);
+  }
+  l.status = take(sizeof(uint32_t) * 256 * size_t(g.maxtiles));
+  l.tasks = take(sizeof(Task) * g.maxtasks);
+  l.keys = take(size_t(g.kb) * g.n);
+  l.vals = take(size_t(g.vb) * g.n);
+  l.total = off;
+  return l;
+}
+
+template <typename F>
+static int max_active(F kernel, int block, size_t smem) {
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, block, smem);
+  return nb > 0 ? nb : 1;
+}
+
+template <typename K, int VB, int KIND>
+static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp, size_t ws_bytes,
+                    cudaStream_t st) {
+  const int kb = int(sizeof(K));
+  const Geometry geo = geometry(n, kb, VB, width_eff);
+  const Layout lay = layout(geo);
+  if (ws_bytes < lay.total)
+    return fail(BS_ERR_WORKSPACE, "workspace too small: need " + std::to_string(lay.total) +
+                                      " bytes, got " + std::to_string(ws_bytes));
+  char *base = static_cast<char *>(wsp);
+  Ws ws{};
+  ws.ctl = reinterpret_cast<Ctl *>(base + lay.ctl);
+  for (int p = 0; p < 2; ++p) {
+    ws.buckets[p] = reinterpret_cast<Bucket *>(base + lay.buckets[p]);
+    ws.bhist[p] = reinterpret_cast<uint32_t *>(base + lay.bhist[p]);
+    ws.bor[p] = reinterpret_cast<uint64_t *>(base + lay.bor[p]);
+    ws.band[p] = reinterpret_cast<uint64_t *>(base + lay.band[p]);
+    ws.tile_bucket[p] = reinterpret_cast<uint32_t *>(base + lay.tile_bucket[p]);
+  }
+  ws.status = reinterpret_cast<uint32_t *>(base + lay.status);
+  ws.tasks = reinterpret_cast<Task *>(base + lay.tasks);
+  ws.keys[0] = keys;
+  ws.keys[1] = base + lay.keys;
+  ws.vals[0] = vals;
+  ws.vals[1] = VB ? base + lay.vals : nullptr;
+  ws.n = n;
+  ws.maxb = geo.maxb;
+  ws.maxtiles = geo.maxtiles;
+  ws.maxtasks = geo.maxtasks;
+  ws.tile = geo.tile;
+  ws.local_max = geo.local_max;
+  ws.group_min = geo.group_min;
+  ws.ndig = geo.ndig;
+  ws.shift0 = int(sizeof(K) * 8) - width_eff;
+
+  constexpr int SKPT = sc_kpt<K>();
+  using SS = ScatterSmem<K, VB, KIND, SC_BLOCK, SKPT>;
+  using LS = LocalSmem<K, VB, KIND, LC_BLOCK, LC_KPT>;
+  auto sc = scatter_kernel<K, VB, KIND, SC_BLOCK, SKPT>;
+  auto lc = local_kernel<K, VB, KIND, LC_BLOCK, LC_KPT>;
+  auto hk = hist_kernel<K, KIND, HI_BLOCK, SKPT * SC_BLOCK / HI_BLOCK>;
+  static int sc_grid = 0, lc_grid = 0, hk_grid = 0;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    cudaError_t e1 = cudaFuncSetAttribute(sc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SS::bytes));
+    cudaError_t e2 = cudaFuncSetAttribute(lc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(LS::bytes));
+    attr_err = e1 != cudaSuccess ? e1 : e2;
+    sc_grid = num_sms() * max_active(sc, SC_BLOCK, SS::bytes);
+    lc_grid = num_sms() * max_active(lc, LC_BLOCK, LS::bytes);
+    hk_grid = num_sms() * max_active(hk, HI_BLOCK, 0);
+  });
+  if (attr_err != cudaSuccess) return fail(BS_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
+
+  BS_CUDA(cudaMemsetAsync(ws.ctl, 0, sizeof(Ctl), st));
+  {
+    const uint32_t ntiles = uint32_t((n + geo.tile - 1) / geo.tile);
+    const int g = int(min64((ntiles + 255) / 256 + 1, 4096));
+    init_kernel<K, KIND><<<g, 256, 0, st>>>(ws);
+  }
+  if (n > geo.local_max) {
+    const int nlev = geo.ndig + 1;
+    for (int L = 0; L < nlev; ++L) {
+      hist_kernel<K, KIND, HI_BLOCK, SKPT * SC_BLOCK / HI_BLOCK><<<hk_grid, HI_BLOCK, 0, st>>>(ws, L);
+      plan_kernel<K><<<num_sms() * 4, 256, 0, st>>>(ws, L);
+      sc<<<sc_grid, SC_BLOCK, SS::bytes, st>>>(ws, L);
+    }
+  }
+  lc<<<lc_grid, LC_BLOCK, LS::bytes, st>>>(ws);
+  BS_CUDA(cudaGetLastError());
+  return BS_OK;
+}
+
+template <typename K, int KIND>
+static int run_metrics(const void *keys, uint64_t n, int width_eff, int64_t depth0, int64_t *counters,
+                       cudaStream_t st) {
+  if (n < 2) return BS_OK;
+  constexpr int BLOCK = 256, IPT = 8;
+  const uint64_t chunks = (n + BLOCK * IPT - 1) / (BLOCK * IPT);
+  const int grid = int(min64(chunks, uint64_t(num_sms()) * 8));
+  metrics_kernel<K, KIND, BLOCK, IPT><<<grid, BLOCK, 0, st>>>(
+      static_cast<const K *>(keys), n, int(sizeof(K) * 8) - width_eff, width_eff, depth0,
+      reinterpret_cast<unsigned long long *>(counters));
+  metrics_root_kernel<<<1, 1, 0, st>>>(reinterpret_cast<unsigned long long *>(counters));
+  BS_CUDA(cudaGetLastError());
+  return BS_OK;
+}
+
+static int check_common(int key_bytes, int val_bytes, int width, int start_pos, int key_kind) {
+  if (key_bytes != 4 && key_bytes != 8) return fail(BS_ERR_VALUE, "key_bytes must be 4 or 8");
+  if (val_bytes != 0 && val_bytes != 4 && val_bytes != 8) return fail(BS_ERR_VALUE, "val_bytes must be 0, 4 or 8");
+  if (width < 1 || width > key_bytes * 8)
+    return fail(BS_ERR_VALUE, "unsupported word width " + std::to_string(width));
+  if (start_pos < 0 || start_pos > width) return fail(BS_ERR_ASSERT, "bit position out of codec width");
+  if (key_kind == BS_KEY_SIGNED && width < 2) return fail(BS_ERR_VALUE, "unsupported word width " + std::to_string(width));
+  if (key_kind == BS_KEY_FLOAT && (key_bytes != 8 || width != 64))
+    return fail(BS_ERR_VALUE, "float keys are 64-bit words of width 64");
+  if (key_kind < 0 || key_kind > 2) return fail(BS_ERR_VALUE, "unknown key_kind");
+  return BS_OK;
+}
+
+}  // namespace bs
+
+using namespace bs;
+
+extern "C" {
+
+int bs_version(void) { return 100; }
+
+const char *bs_last_error(void) { return g_err.c_str(); }
+
+size_t bs_workspace_bytes(uint64_t n, int key_bytes, int val_bytes) {
+  if ((key_bytes != 4 && key_bytes != 8) || (val_bytes != 0 && val_bytes != 4 && val_bytes != 8)) return 0;
+  return layout(geometry(n, key_bytes, val_bytes, key_bytes * 8)).total;
+}
+
+int bs_sort(void *keys, void *vals, uint64_t n, int key_bytes, int val_bytes, int width, int start_pos,
+            int key_kind, void *ws, size_t ws_bytes, void *stream, int64_t *counters, int64_t depth) {
+  int rc = check_common(key_bytes, val_bytes, width, start_pos, key_kind);
+  if (rc) return rc;
+  if (val_bytes != 0 && vals == nullptr) return fail(BS_ERR_VALUE, "val_bytes > 0 but vals is NULL");
+  if (n >= (uint64_t(1) << 30) + 1) return fail(BS_ERR_VALUE, "n > 2^30 elements per call is not supported");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int width_eff = width - start_pos;
+  // the sign bit lies above the effective key once start_pos > 0
+  if (key_kind == BS_KEY_SIGNED && start_pos > 0) key_kind = BS_KEY_UNSIGNED;
+  if (counters) BS_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(int64_t), st));
+  if (n <= 1 || width_eff == 0) return BS_OK;
+  if (val_bytes == 0) vals = nullptr;
+#define BS_DISPATCH_V(K, KIND)                                                                  \
+  do {                                                                                          \
+    if (val_bytes == 0) rc = run_sort<K, 0, KIND>(keys, vals, n, width_eff, ws, ws_bytes, st);  \
+    else if (val_bytes == 4) rc = run_sort<K, 4, KIND>(keys, vals, n, width_eff, ws, ws_bytes, st); \
+    else rc = run_sort<K, 8, KIND>(keys, vals, n, width_eff, ws, ws_bytes, st);                 \
+  } while (0)
+  if (key_bytes == 4) {
+    if (key_kind == BS_KEY_UNSIGNED) BS_DISPATCH_V(uint32_t, 0);
+    else BS_DISPATCH_V(uint32_t, 1);
+  } else {
+    if (key_kind == BS_KEY_UNSIGNED) BS_DISPATCH_V(uint64_t, 0);
+    else if (key_kind == BS_KEY_SIGNED) BS_DISPATCH_V(uint64_t, 1);
+    else BS_DISPATCH_V(uint64_t, 2);
+  }
+#undef BS_DISPATCH_V
+  if (rc) return rc;
+  if (counters) return bs_metrics(keys, n, key_bytes, width, start_pos, key_kind, depth, nullptr, 0, stream, counters);
+  return BS_OK;
+}
+
+size_t bs_metrics_workspace_bytes(uint64_t) { return 0; }
+
+int bs_metrics(const void *sorted_keys, uint64_t n, int key_bytes, int width, int start_pos, int key_kind,
+               int64_t depth, void *, size_t, void *stream, int64_t *counters) {
+  int rc = check_common(key_bytes, 0, width, start_pos, key_kind);
+  if (rc) return rc;
+  if (!counters) return fail(BS_ERR_VALUE, "counters is NULL");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int width_eff = width - start_pos;
+  if (key_kind == BS_KEY_SIGNED && start_pos > 0) key_kind = BS_KEY_UNSIGNED;
+  if (n < 2 || width_eff == 0) return BS_OK;
+  if (key_bytes == 4) {
+    if (key_kind == BS_KEY_UNSIGNED) return run_metrics<uint32_t, 0>(sorted_keys, n, width_eff, depth, counters, st);
+    return run_metrics<uint32_t, 1>(sorted_keys, n, width_eff, depth, counters, st);
+  }
+  if (key_kind == BS_KEY_UNSIGNED) return run_metrics<uint64_t, 0>(sorted_keys, n, width_eff, depth, counters, st);
+  if (key_kind == BS_KEY_SIGNED) return run_metrics<uint64_t, 1>(sorted_keys, n, width_eff, depth, counters, st);
+  return run_metrics<uint64_t, 2>(sorted_keys, n, width_eff, depth, counters, st);
+}
+
+size_t bs_partition_workspace_bytes(uint64_t n, int key_bytes, int val_bytes) {
+  const uint64_t nblk = (n + PART_CHUNK - 1) / PART_CHUNK;
+  return align_up(size_t(key_bytes) * n) + align_up(size_t(val_bytes) * n) +
+         2 * align_up(sizeof(uint32_t) * (n + 1)) + align_up(sizeof(uint32_t) * (nblk + 1)) + 256;
+}
+
+int bs_partition_words(void *keys, void *vals, uint64_t n, int key_bytes, int val_bytes, int width, int pos,
+                       void *ws, size_t ws_bytes, void *stream, int64_t *split_dev, int64_t *counters) {
+  if (key_bytes != 4 && key_bytes != 8) return fail(BS_ERR_VALUE, "key_bytes must be 4 or 8");
+  if (val_bytes != 0 && val_bytes != 4 && val_bytes != 8) return fail(BS_ERR_VALUE, "val_bytes must be 0, 4 or 8");
+  if (val_bytes != 0 && vals == nullptr) return fail(BS_ERR_VALUE, "val_bytes > 0 but vals is NULL");
+  if (width < 1 || width > 64) return fail(BS_ERR_VALUE, "unsupported word width");
+  if (n == 0) return fail(BS_ERR_ASSERT, "partition requires a non-empty range");
+  if (pos < 0 || pos >= width) return fail(BS_ERR_ASSERT, "bit position out of codec width");
+  if (n >= (uint64_t(1) << 32)) return fail(BS_ERR_VALUE, "n too large");
+  if (ws_bytes < bs_partition_workspace_bytes(n, key_bytes, val_bytes))
+    return fail(BS_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  char *b = static_cast<char *>(ws);
+  void *copy = b;
+  b += align_up(size_t(key_bytes) * n);
+  void *vcopy = b;
+  b += align_up(size_t(val_bytes) * n);
+  uint32_t *lone = reinterpret_cast<uint32_t *>(b);
+  b += align_up(sizeof(uint32_t) * (n + 1));
+  uint32_t *zpos = reinterpret_cast<uint32_t *>(b);
+  b += align_up(sizeof(uint32_t) * (n + 1));
+  uint32_t *bcnt = reinterpret_cast<uint32_t *>(b);
+  const uint64_t nblk = (n + PART_CHUNK - 1) / PART_CHUNK;
+  uint32_t *Zp = bcnt + nblk;
+  BS_CUDA(cudaMemcpyAsync(copy, keys, size_t(key_bytes) * n, cudaMemcpyDeviceToDevice, st));
+  if (val_bytes) BS_CUDA(cudaMemcpyAsync(vcopy, vals, size_t(val_bytes) * n, cudaMemcpyDeviceToDevice, st));
+  auto go = [&](auto tag, auto vbc) -> int {
+    using K = decltype(tag);
+    constexpr int VB = decltype(vbc)::value;
+    const K *src = static_cast<const K *>(copy);
+    part_count_kernel<K><<<unsigned(nblk), PART_BLOCK, 0, st>>>(src, n, pos, width, bcnt);
+    scan_blocks_kernel<<<1, 1024, 0, st>>>(bcnt, uint32_t(nblk), Zp);
+    part_index_kernel<K><<<unsigned(nblk), PART_BLOCK, 0, st>>>(src, n, pos, width, bcnt, Zp, lone, zpos);
+    part_gather_kernel<K, VB><<<unsigned(nblk), PART_BLOCK, 0, st>>>(src, static_cast<K *>(keys), vcopy, vals, n,
+                                                                     pos, width, bcnt, Zp, lone, zpos);
+    part_finish_kernel<<<1, 1, 0, st>>>(Zp, n, split_dev, reinterpret_cast<unsigned long long *>(counters));
+    BS_CUDA(cudaGetLastError());
+    return BS_OK;
+  };
+  using I0 = std::integral_constant<int, 0>;
+  using I4 = std::integral_constant<int, 4>;
+  using I8 = std::integral_constant<int, 8>;
+  if (key_bytes == 4) {
+    if (val_bytes == 0) return go(uint32_t(0), I0{});
+    if (val_bytes == 4) return go(uint32_t(0), I4{});
+    return go(uint32_t(0), I8{});
+  }
+  if (val_bytes == 0) return go(uint64_t(0), I0{});
+  if (val_bytes == 4) return go(uint64_t(0), I4{});
+  return go(uint64_t(0), I8{});
+}
+
+int bs_range_sorted(const void *keys, uint64_t n, int key_bytes, void *stream, int32_t *flag_dev) {
+  if (key_bytes != 4 && key_bytes != 8) return fail(BS_ERR_VALUE, "key_bytes must be 4 or 8");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int32_t one = 1;
+  BS_CUDA(cudaMemcpyAsync(flag_dev, &one, sizeof(one), cudaMemcpyHostToDevice, st));
+  if (n < 2) return BS_OK;
+  const int grid = int(min64((n + 255) / 256, uint64_t(num_sms()) * 8));
+  if (key_bytes == 4)
+    range_sorted_kernel<uint32_t><<<grid, 256, 0, st>>>(static_cast<const uint32_t *>(keys), n, flag_dev);
+  else
+    range_sorted_kernel<uint64_t><<<grid, 256, 0, st>>>(static_cast<const uint64_t *>(keys), n, flag_dev);
+  BS_CUDA(cudaGetLastError());
+  return BS_OK;
+}
+
+size_t bs_split_workspace_bytes(uint64_t n, int, int, int) {
+  const uint64_t ntiles = (n + SPLIT_TILE - 1) / SPLIT_TILE;
+  return align_up(sizeof(uint32_t) * 16 * (ntiles + 1));
+}
+
+int bs_split_by_splitters(const void *keys, const void *vals, uint64_t n, int key_bytes, int val_bytes,
+                          int width, int key_kind, const void *splitters, int nranks, void *out_keys,
+                          void *out_vals, uint64_t *class_counts, void *ws, size_t ws_bytes, void *stream) {
+  int rc = check_common(key_bytes, val_bytes, width, 0, key_kind);
+  if (rc) return rc;
+  if (nranks < 1 || nranks > 8) return fail(BS_ERR_VALUE, "nranks must be in [1, 8]");
+  if (n >= (uint64_t(1) << 32)) return fail(BS_ERR_VALUE, "n too large");
+  if (ws_bytes < bs_split_workspace_bytes(n, key_bytes, val_bytes, nranks))
+    return fail(BS_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int ncls = 2 * nranks - 1, nsp = nranks - 1;
+  BS_CUDA(cudaMemsetAsync(class_counts, 0, sizeof(uint64_t) * ncls, st));
+  if (n == 0) return BS_OK;
+  const uint32_t ntiles = uint32_t((n + SPLIT_TILE - 1) / SPLIT_TILE);
+  uint32_t *tile_hist = static_cast<uint32_t *>(ws);
+  const int shift0 = key_bytes * 8 - width;
+  auto go = [&](auto ktag, auto kindc, auto vbc) -> int {
+    using K = decltype(ktag);
+    constexpr int KIND = decltype(kindc)::value;
+    constexpr int VB = decltype(vbc)::value;
+    split_hist_kernel<K, KIND><<<ntiles, SPLIT_BLOCK, 0, st>>>(static_cast<const K *>(keys), n, shift0,
+                                                               static_cast<const K *>(splitters), nsp, tile_hist);
+    split_scan_kernel<<<1, 32, 0, st>>>(tile_hist, ntiles, ncls, reinterpret_cast<unsigned long long *>(class_counts));
+    split_scatter_kernel<K, VB, KIND><<<ntiles, SPLIT_BLOCK, 0, st>>>(
+        static_cast<const K *>(keys), vals, n, shift0, static_cast<const K *>(splitters), nsp, tile_hist,
+        static_cast<K *>(out_keys), out_vals);
+    BS_CUDA(cudaGetLastError());
+    return BS_OK;
+  };
+  using I0 = std::integral_constant<int, 0>;
+  using I1 = std::integral_constant<int, 1>;
+  using I2 = std::integral_constant<int, 2>;
+  using I4 = std::integral_constant<int, 4>;
+  using I8 = std::integral_constant<int, 8>;
+  auto by_v = [&](auto ktag, auto kindc) -> int {
+    if (val_bytes == 0) return go(ktag, kindc, I0{});
+    if (val_bytes == 4) return go(ktag, kindc, I4{});
+    return go(ktag, kindc, I8{});
+  };
+  if (key_bytes == 4) return key_kind == 0 ? by_v(uint32_t(0), I0{}) : by_v(uint32_t(0), I1{});
+  if (key_kind == 0) return by_v(uint64_t(0), I0{});
+  if (key_kind == 1) return by_v(uint64_t(0), I1{});
+  return by_v(uint64_t(0), I2{});
+}
+
+int bs_sample_keys(const void *keys, uint64_t n, int key_bytes, int width, int key_kind, uint64_t count,
+                   void *out_samples, void *stream) {
+  int rc = check_common(key_bytes, 0, width, 0, key_kind);
+  if (rc) return rc;
+  if (n == 0 || count == 0) return BS_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int shift0 = key_bytes * 8 - width;
+  const int grid = int(min64((count + 255) / 256, 1024));
+  if (key_bytes == 4) {
+    if (key_kind == 0)
+      sample_kernel<uint32_t, 0><<<grid, 256, 0, st>>>(static_cast<const uint32_t *>(keys), n, shift0, count,
+                                                      static_cast<uint32_t *>(out_samples));
+    else
+      sample_kernel<uint32_t, 1><<<grid, 256, 0, st>>>(static_cast<const uint32_t *>(keys), n, shift0, count,
+                                                      static_cast<uint32_t *>(out_samples));
+  } else {
+    if (key_kind == 0)
+      sample_kernel<uint64_t, 0><<<grid, 256, 0, st>>>(static_cast<const uint64_t *>(keys), n, shift0, count,
+                                                      static_cast<uint64_t *>(out_samples));
+    else if (key_kind == 1)
+      sample_kernel<uint64_t, 1><<<grid, 256, 0, st>>>(static_cast<const uint64_t *>(keys), n, shift0, count,
+                                                      static_cast<uint64_t *>(out_samples));
+    else
+      sample_kernel<uint64_t, 2><<<grid, 256, 0, st>>>(static_cast<const uint64_t *>(keys), n, shift0, count,
+                                                      static_cast<uint64_t *>(out_samples));
+  }
+  BS_CUDA(cudaGetLastError());
+  return BS_OK;
+}
+
+}  // extern "C"

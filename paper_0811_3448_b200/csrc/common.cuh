@@ -1,0 +1,180 @@
+// common.cuh -- shared device helpers for the Binar Sort sm_100a kernels.
+//
+// Key model (reference semantics, keys.py:35-93, kernels.py:63,69):
+//   * a word x of W bits carries its sort key in the low `width` bits, read
+//     MSB-first from bit width-1 (UnsignedCodec), after the codec transform
+//     (SignedCodec: flip the sign bit; Float64Codec: IEEE total order);
+//   * the GPU works on the *normalised encoded key* nk = enc(x) << (W-width),
+//     so digit j (0 = most significant) is (nk >> (W-8-8j)) & 0xFF.  A
+//     digit pass over 8 bits computes exactly the buckets that 8 levels of
+//     the reference's binary recursion compute (SURVEY §7 design sketch).
+//   * the data moved is always the raw word x: no transform passes.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bs {
+
+constexpr int WARP = 32;
+
+template <int VB> struct ValT { using T = uint32_t; };
+template <> struct ValT<8> { using T = uint64_t; };
+
+__host__ __device__ __forceinline__ uint64_t min64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+template <typename K> struct KeyTraits;
+template <> struct KeyTraits<uint32_t> {
+  static constexpr int BITS = 32;
+  __device__ __forceinline__ static int clz(uint32_t x) { return __clz(x); }
+};
+template <> struct KeyTraits<uint64_t> {
+  static constexpr int BITS = 64;
+  __device__ __forceinline__ static int clz(uint64_t x) { return __clzll(x); }
+};
+
+// Codec transform, keys.py:51-93.  KIND 0 unsigned, 1 signed, 2 float.
+template <typename K, int KIND>
+__device__ __forceinline__ K encode(K x) {
+  constexpr int W = KeyTraits<K>::BITS;
+  constexpr K MSB = K(1) << (W - 1);
+  if constexpr (KIND == 0) {
+    return x;
+  } else if constexpr (KIND == 1) {
+    return x ^ MSB;
+  } else {
+    K m = K(0) - (x >> (W - 1));  // all ones iff sign bit set
+    return x ^ (m | MSB);
+  }
+}
+
+// Per-launch view of the key geometry.
+template <typename K, int KIND>
+struct KeyGeom {
+  int shift0;  // W - width_eff
+  // SignedCodec(width) flips bit width-1 of the low-width word (keys.py:51-58):
+  // after the shift that is the word's top bit, so any width works.
+  __device__ __forceinline__ K norm(K x) const {
+    constexpr K MSB = K(1) << (KeyTraits<K>::BITS - 1);
+    if constexpr (KIND == 0) return x << shift0;
+    else if constexpr (KIND == 1) return (x << shift0) ^ MSB;
+    else return encode<K, KIND>(x) << shift0;
+  }
+  __device__ __forceinline__ static uint32_t digit_of_norm(K nk, int dig) {
+    constexpr int W = KeyTraits<K>::BITS;
+    return uint32_t(nk >> (W - 8 - 8 * dig)) & 0xFFu;
+  }
+  __device__ __forceinline__ uint32_t digit(K x, int dig) const {
+    return digit_of_norm(norm(x), dig);
+  }
+};
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint32_t *p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Peers of this lane among the lanes in `active` that hold the same 8-bit
+// digit: 8 warp ballots, one per bit plane (the north_star's ballot/popc
+// ranking).  Result includes the lane itself when it is active.
+__device__ __forceinline__ uint32_t match_digit8(uint32_t d, uint32_t active) {
+  uint32_t peers = active;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    const bool bit = (d >> b) & 1u;
+    const uint32_t bb = __ballot_sync(0xFFFFFFFFu, bit);
+    peers &= bit ? bb : ~bb;
+  }
+  return peers;
+}
+
+// Stable warp-level ranking of KPT elements per lane by 8-bit digit.
+// Element layout: chunk j / lane l  <->  warp-local index 32*j + l.
+// whist: this warp's 256 counters in shared memory, zero on entry; on exit
+// whist[d] = number of this warp's valid elements with digit d.
+// rank[j] = stable rank of element (j, lane) among this warp's elements of
+// the same digit.  `nvalid` = number of valid warp-local elements (prefix).
+template <int KPT>
+__device__ __forceinline__ void warp_rank(const uint32_t (&dig)[KPT], int nvalid,
+                                          uint32_t *whist, uint32_t (&rank)[KPT]) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) {
+    const int idx = 32 * j + lane;
+    const bool valid = idx < nvalid;
+    if (32 * j >= nvalid) {  // warp-uniform: nothing left
+      rank[j] = 0;
+      continue;
+    }
+    const uint32_t active = __ballot_sync(0xFFFFFFFFu, valid);
+    const uint32_t d = dig[j];
+    const uint32_t peers = match_digit8(d, active);
+    const uint32_t below = __popc(peers & lt);
+    uint32_t old = 0;
+    if (valid && below == 0) {
+      old = whist[d];
+      whist[d] = old + __popc(peers);
+    }
+    const int leader = __ffs(peers) - 1;
+    old = __shfl_sync(0xFFFFFFFFu, old, valid ? leader : lane);
+    rank[j] = old + below;
+    __syncwarp();
+  }
+}
+
+// Block-wide exclusive scan of one value per thread for the first 256 threads
+// (digit counts).  `scratch` needs 256/32 + 1 words.  Returns the exclusive
+// prefix; *total (optional) gets the sum.  All BLOCK threads must call.
+template <int BLOCK>
+__device__ __forceinline__ uint32_t scan256_excl(uint32_t v, uint32_t *scratch) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  uint32_t x = (tid < 256) ? v : 0u;
+  uint32_t incl = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (tid < 256 && lane == 31) scratch[w] = incl;
+  __syncthreads();
+  if (tid < 32) {
+    uint32_t s = (lane < 8) ? scratch[lane] : 0u;
+    uint32_t si = s;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xFFFFFFFFu, si, o);
+      if (lane >= o) si += y;
+    }
+    if (lane < 8) scratch[lane] = si - s;
+  }
+  __syncthreads();
+  uint32_t r = (tid < 256) ? scratch[w] + incl - x : 0u;
+  __syncthreads();
+  return r;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_or(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v |= __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_and(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v &= __shfl_xor_sync(0xFFFFFFFFu, v, o);
+  return v;
+}
+
+}  // namespace bs

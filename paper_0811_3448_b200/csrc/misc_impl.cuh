@@ -1,0 +1,330 @@
+// misc_impl.cuh -- the smaller kernels of the C ABI:
+//   * exact reference partition pass (kernels.partition_words, kernels.py:56-77)
+//     through its closed form;
+//   * range_sorted_words (kernels.py:80-85);
+//   * multi-GPU front-end device steps: strided key sampling and a stable
+//     partition into 2R-1 splitter classes (replaces variants._prepartition,
+//     variants.py:124-148, as the step before the NCCL all-to-all-v).
+#pragma once
+
+#include "common.cuh"
+
+namespace bs {
+
+// ---------------------------------------------------------------------------
+// Simple device scan of per-block counts (reduce-then-scan, one CTA).
+// ---------------------------------------------------------------------------
+__global__ void scan_blocks_kernel(uint32_t *counts, uint32_t nblocks, uint32_t *total) {
+  // exclusive scan in place, single CTA of 1024 threads
+  __shared__ uint32_t s[1024];
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base < nblocks; base += 1024) {
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t v = (i < nblocks) ? counts[i] : 0u;
+    s[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+      uint32_t t = (int(threadIdx.x) >= o) ? s[threadIdx.x - o] : 0u;
+      __syncthreads();
+      s[threadIdx.x] += t;
+      __syncthreads();
+    }
+    if (i < nblocks) counts[i] = carry + s[threadIdx.x] - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += s[1023];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && total) *total = carry;
+}
+
+// ---------------------------------------------------------------------------
+// Exact partition pass.  With b_i the bit of element i at `pos` and Z the
+// number of zeros (split = Z):
+//  * zero region i < Z: keeps e_i if b_i == 0; the k-th L-one (bit-1 element
+//    at a position < Z) is replaced by the k-th R-zero (bit-0 element at a
+//    position >= Z, counted from the right end);
+//  * one region: offset n-1 gets L-one #0; offset q-1 (Z < q <= n-1) gets e_q
+//    if b_q == 1, else L-one #(1 + #zeros in (q, n)).
+// swaps = n - Z (every bit-1 element is swapped exactly once), extractions = n.
+// ---------------------------------------------------------------------------
+constexpr int PART_BLOCK = 256;
+constexpr int PART_IPT = 16;
+constexpr int PART_CHUNK = PART_BLOCK * PART_IPT;
+
+template <typename K>
+__device__ __forceinline__ uint32_t bit_at(K x, int pos, int width) {
+  // (u64(x) << pos) & (1 << (width-1)), kernels.py:63,69
+  const uint64_t msb = uint64_t(1) << (width - 1);
+  return ((uint64_t(x) << pos) & msb) ? 1u : 0u;
+}
+
+template <typename K>
+__global__ void part_count_kernel(const K *keys, uint64_t n, int pos, int width, uint32_t *bcount) {
+  __shared__ uint32_t s[PART_BLOCK / 32];
+  const uint64_t base = uint64_t(blockIdx.x) * PART_CHUNK;
+  uint32_t c = 0;
+  for (int j = 0; j < PART_IPT; ++j) {
+    const uint64_t i = base + uint64_t(j) * PART_BLOCK + threadIdx.x;
+    if (i < n) c += bit_at(keys[i], pos, width) ^ 1u;  // zeros
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, o);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int i = 0; i < PART_BLOCK / 32; ++i) t += s[i];
+    bcount[blockIdx.x] = t;
+  }
+}
+
+// exclusive zero-prefix per element, computed per chunk sequentially per
+// thread-block (chunk order = element order): block-level scan of zeros.
+template <typename K>
+__device__ __forceinline__ void chunk_zero_prefix(const K *keys, uint64_t n, int pos, int width,
+                                                  uint32_t block_excl, uint32_t (&zp)[PART_IPT],
+                                                  uint32_t (&bit)[PART_IPT], uint32_t *s_warp) {
+  // thread t owns elements base + t*IPT + j (blocked, contiguous per thread)
+  const uint64_t base = uint64_t(blockIdx.x) * PART_CHUNK + uint64_t(threadIdx.x) * PART_IPT;
+  uint32_t run = 0;
+  for (int j = 0; j < PART_IPT; ++j) {
+    const uint64_t i = base + j;
+    bit[j] = (i < n) ? bit_at(keys[i], pos, width) : 1u;
+    zp[j] = run;
+    run += (i < n) ? (bit[j] ^ 1u) : 0u;
+  }
+  // block exclusive scan of `run`
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t incl = run;
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_warp[w] = incl;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t acc = 0;
+    for (int i = 0; i < PART_BLOCK / 32; ++i) {
+      uint32_t t = s_warp[i];
+      s_warp[i] = acc;
+      acc += t;
+    }
+  }
+  __syncthreads();
+  const uint32_t texcl = block_excl + s_warp[w] + incl - run;
+  for (int j = 0; j < PART_IPT; ++j) zp[j] += texcl;
+}
+
+// zp = #zeros in [0, i).  For i < Z: #ones in [0,i) = i - zp.  For i >= Z:
+// #zeros in (i, n) = Z - zp - (b_i==0).
+template <typename K>
+__global__ void part_index_kernel(const K *keys, uint64_t n, int pos, int width,
+                                  const uint32_t *bexcl, const uint32_t *Zp, uint32_t *lone,
+                                  uint32_t *zpos) {
+  __shared__ uint32_t s_warp[PART_BLOCK / 32];
+  uint32_t zp[PART_IPT], bit[PART_IPT];
+  chunk_zero_prefix(keys, n, pos, width, bexcl[blockIdx.x], zp, bit, s_warp);
+  const uint32_t Z = *Zp;
+  const uint64_t base = uint64_t(blockIdx.x) * PART_CHUNK + uint64_t(threadIdx.x) * PART_IPT;
+  for (int j = 0; j < PART_IPT; ++j) {
+    const uint64_t i = base + j;
+    if (i >= n) break;
+    // L-ones: bit-1 elements the low cursor examines fresh, i.e. positions
+    // [0, Z] (position Z only when it holds a one); rank = #ones before.
+    if (i <= Z && bit[j]) lone[uint32_t(i) - zp[j]] = uint32_t(i);
+    // R-zeros: bit-0 elements at positions >= Z, ranked from the right end.
+    if (i >= Z && !bit[j]) zpos[Z - zp[j] - 1u] = uint32_t(i);
+  }
+}
+
+template <typename K, int VB>
+__global__ void part_gather_kernel(const K *src, K *dst, const void *vsrc_, void *vdst_, uint64_t n,
+                                   int pos, int width, const uint32_t *bexcl, const uint32_t *Zp,
+                                   const uint32_t *lone, const uint32_t *zpos) {
+  using V = typename ValT<VB>::T;
+  const V *vsrc = static_cast<const V *>(vsrc_);
+  V *vdst = static_cast<V *>(vdst_);
+  auto mv = [&](uint64_t to, uint64_t from) {
+    dst[to] = src[from];
+    if constexpr (VB != 0) vdst[to] = vsrc[from];
+  };
+  __shared__ uint32_t s_warp[PART_BLOCK / 32];
+  uint32_t zp[PART_IPT], bit[PART_IPT];
+  chunk_zero_prefix(src, n, pos, width, bexcl[blockIdx.x], zp, bit, s_warp);
+  const uint32_t Z = *Zp;
+  const uint64_t base = uint64_t(blockIdx.x) * PART_CHUNK + uint64_t(threadIdx.x) * PART_IPT;
+  for (int j = 0; j < PART_IPT; ++j) {
+    const uint64_t i = base + j;
+    if (i >= n) break;
+    if (i < Z) {
+      mv(i, bit[j] ? uint64_t(zpos[uint32_t(i) - zp[j]]) : i);
+    } else {
+      // element i is q for target offset q-1 (q > Z); offset n-1 handled below
+      if (i > Z) {
+        const uint32_t zeros_after = Z - zp[j] - (bit[j] ^ 1u);
+        mv(i - 1, bit[j] ? i : uint64_t(lone[1u + zeros_after]));
+      }
+      if (i == n - 1) mv(n - 1, lone[0]);
+    }
+  }
+}
+
+__global__ void part_finish_kernel(const uint32_t *Zp, uint64_t n, int64_t *split,
+                                   unsigned long long *counters) {
+  const uint32_t Z = *Zp;
+  if (split) *split = int64_t(Z);
+  if (counters) {
+    atomicAdd(&counters[0], (unsigned long long)n);
+    atomicAdd(&counters[1], (unsigned long long)(n - Z));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// range_sorted_words: flag stays 1 unless some adjacent pair is decreasing.
+// ---------------------------------------------------------------------------
+template <typename K>
+__global__ void range_sorted_kernel(const K *keys, uint64_t n, int32_t *flag) {
+  bool ok = true;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i + 1 < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    ok &= !(keys[i] > keys[i + 1]);
+  if (!__all_sync(0xFFFFFFFFu, ok) && (threadIdx.x & 31) == 0) *flag = 0;
+}
+
+// ---------------------------------------------------------------------------
+// Multi-GPU helpers.
+// ---------------------------------------------------------------------------
+template <typename K, int KIND>
+__global__ void sample_kernel(const K *keys, uint64_t n, int shift0, uint64_t count, K *out) {
+  const KeyGeom<K, KIND> g{shift0};
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t idx = ((2 * i + 1) * n) / (2 * count);
+    out[i] = g.norm(keys[idx]);
+  }
+}
+
+// class of a normalised key against R-1 sorted normalised splitters:
+// 2j (strictly between s_{j-1} and s_j) or 2j+1 (equal to s_j)
+template <typename K>
+__device__ __forceinline__ uint32_t split_class(K nk, const K *spl, int nsp) {
+  uint32_t c = 0;
+  for (int j = 0; j < nsp; ++j) {
+    const K s = spl[j];
+    c += (nk > s) ? 2u : (nk == s ? 1u : 0u);
+  }
+  return c;
+}
+
+constexpr int SPLIT_BLOCK = 256;
+constexpr int SPLIT_KPT = 16;
+constexpr int SPLIT_TILE = SPLIT_BLOCK * SPLIT_KPT;
+
+template <typename K, int KIND>
+__global__ void split_hist_kernel(const K *keys, uint64_t n, int shift0, const K *spl, int nsp,
+                                  uint32_t *tile_hist /* [ntiles][16] */) {
+  const KeyGeom<K, KIND> g{shift0};
+  __shared__ uint32_t h[16];
+  __shared__ K s_spl[16];
+  if (threadIdx.x < 16) h[threadIdx.x] = 0;
+  if (threadIdx.x < nsp) s_spl[threadIdx.x] = spl[threadIdx.x];
+  __syncthreads();
+  const uint64_t base = uint64_t(blockIdx.x) * SPLIT_TILE;
+  for (int j = 0; j < SPLIT_KPT; ++j) {
+    const uint64_t i = base + uint64_t(j) * SPLIT_BLOCK + threadIdx.x;
+    if (i < n) atomicAdd(&h[split_class(g.norm(keys[i]), s_spl, nsp)], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < 16) tile_hist[size_t(blockIdx.x) * 16 + threadIdx.x] = h[threadIdx.x];
+}
+
+// one CTA: class-major exclusive scan over (class, tile) -> absolute offsets
+__global__ void split_scan_kernel(uint32_t *tile_hist, uint32_t ntiles, int ncls,
+                                  unsigned long long *class_counts) {
+  __shared__ unsigned long long tot[16];
+  const int c = threadIdx.x;
+  if (c < 16) {
+    unsigned long long s = 0;
+    if (c < ncls)
+      for (uint32_t t = 0; t < ntiles; ++t) s += tile_hist[size_t(t) * 16 + c];
+    tot[c] = s;
+  }
+  __syncthreads();
+  if (c < ncls) {
+    unsigned long long base = 0;
+    for (int i = 0; i < c; ++i) base += tot[i];
+    for (uint32_t t = 0; t < ntiles; ++t) {
+      const uint32_t v = tile_hist[size_t(t) * 16 + c];
+      tile_hist[size_t(t) * 16 + c] = uint32_t(base);
+      base += v;
+    }
+    class_counts[c] = tot[c];
+  }
+}
+
+template <typename K, int VB, int KIND>
+__global__ void __launch_bounds__(SPLIT_BLOCK) split_scatter_kernel(
+    const K *keys, const void *vals_, uint64_t n, int shift0, const K *spl, int nsp,
+    const uint32_t *tile_off, K *out_keys, void *out_vals_) {
+  using V = typename ValT<VB>::T;
+  const V *vals = static_cast<const V *>(vals_);
+  V *out_vals = static_cast<V *>(out_vals_);
+  constexpr int NW = SPLIT_BLOCK / 32;
+  const KeyGeom<K, KIND> g{shift0};
+  __shared__ uint32_t whist_all[NW * 256];
+  __shared__ uint32_t tstart[256];
+  __shared__ uint32_t misc[32];
+  __shared__ K s_spl[16];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid < nsp) s_spl[tid] = spl[tid];
+  uint32_t *whist = whist_all + w * 256;
+  for (int i = lane; i < 256; i += 32) whist[i] = 0;
+  __syncthreads();
+  const uint64_t base = uint64_t(blockIdx.x) * SPLIT_TILE;
+  const int cnt = int(min64(SPLIT_TILE, n - base));
+  const int wbase = w * 32 * SPLIT_KPT;
+  const int nvw = max(0, min(32 * SPLIT_KPT, cnt - wbase));
+  K x[SPLIT_KPT];
+  V v[SPLIT_KPT];
+  uint32_t dg[SPLIT_KPT], rk[SPLIT_KPT];
+#pragma unroll
+  for (int j = 0; j < SPLIT_KPT; ++j) {
+    const int e = wbase + 32 * j + lane;
+    x[j] = 0;
+    dg[j] = 0;
+    if (e < cnt) {
+      x[j] = keys[base + e];
+      if constexpr (VB != 0) v[j] = vals[base + e];
+      dg[j] = split_class(g.norm(x[j]), s_spl, nsp);
+    }
+  }
+  warp_rank<SPLIT_KPT>(dg, nvw, whist, rk);
+  __syncthreads();
+  uint32_t total = 0;
+  if (tid < 256) {
+    uint32_t s = 0;
+    for (int ww = 0; ww < NW; ++ww) {
+      const uint32_t cc = whist_all[ww * 256 + tid];
+      whist_all[ww * 256 + tid] = s;
+      s += cc;
+    }
+    total = s;
+  }
+  (void)total;
+  __syncthreads();
+  if (tid < 16) tstart[tid] = tile_off[size_t(blockIdx.x) * 16 + tid];
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < SPLIT_KPT; ++j) {
+    const int e = wbase + 32 * j + lane;
+    if (e < cnt) {
+      const uint32_t d = dg[j];
+      const uint64_t o = uint64_t(tstart[d]) + whist[d] + rk[j];
+      out_keys[o] = x[j];
+      if constexpr (VB != 0) out_vals[o] = v[j];
+    }
+  }
+}
+
+}  // namespace bs
