@@ -78,6 +78,21 @@ int bs_sort(void *keys, void *vals, uint64_t n, int key_bytes, int val_bytes,
             void *stream, int64_t *counters, int64_t depth);
 
 /*
+ * bs_sort plus phase timing (bench instrumentation; SYNCHRONISES `stream`):
+ * times the phases [init, {hist(L), plan(L), scatter(L)} for each level L,
+ * local sort] with CUDA events on `stream`, writes up to `nphases` durations
+ * in milliseconds to phase_ms and the number written to *nrecorded.
+ */
+int bs_sort_profiled(void *keys, void *vals, uint64_t n, int key_bytes,
+                     int val_bytes, int width, int start_pos, int key_kind,
+                     void *ws, size_t ws_bytes, void *stream, int64_t *counters,
+                     int64_t depth, float *phase_ms, int nphases, int *nrecorded);
+
+/* Number of kernels bs_sort launches for this shape (for launch accounting). */
+int bs_sort_launches(uint64_t n, int key_bytes, int width, int start_pos,
+                     int with_counters);
+
+/*
  * Reference Metrics of kernels.sort_words over an ALREADY SORTED device array
  * (the K6 closed form).  Adds into the device int64[4]
  * `counters` with Metrics.merge semantics (core.py:60-77): counts add,

@@ -32,7 +32,7 @@ EXPORTS = (
     "bs_version", "bs_last_error", "bs_workspace_bytes", "bs_sort",
     "bs_metrics_workspace_bytes", "bs_metrics", "bs_partition_workspace_bytes",
     "bs_partition_words", "bs_range_sorted", "bs_split_workspace_bytes",
-    "bs_split_by_splitters", "bs_sample_keys",
+    "bs_split_by_splitters", "bs_sample_keys", "bs_sort_profiled", "bs_sort_launches",
 )
 
 
@@ -100,6 +100,11 @@ def lib() -> ctypes.CDLL:
         L.bs_split_by_splitters.restype = i32
         L.bs_sample_keys.argtypes = [vp, u64, i32, i32, i32, u64, vp, vp]
         L.bs_sample_keys.restype = i32
+        L.bs_sort_profiled.argtypes = [vp, vp, u64, i32, i32, i32, i32, i32, vp, sz, vp, vp, i64,
+                                       ctypes.POINTER(ctypes.c_float), i32, ctypes.POINTER(i32)]
+        L.bs_sort_profiled.restype = i32
+        L.bs_sort_launches.argtypes = [u64, i32, i32, i32, i32]
+        L.bs_sort_launches.restype = i32
         _lib = L
         return L
 

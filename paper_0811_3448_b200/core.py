@@ -121,7 +121,8 @@ class DeviceWords:
             src_dtype = src.dtype
 
             def wb():
-                view.copy_(dev.view(src_dtype).to(view.device).to(view.dtype))
+                res = dev.view(src_dtype)
+                view.copy_(res if res.dtype == view.dtype else res.to(view.dtype))  # D2H straight into view
 
             self._chain(wb)
             return dev

@@ -18,6 +18,13 @@ namespace bs {
 
 static thread_local std::string g_err;
 
+// Optional phase events (bs_sort_profiled): thread-local, set for one call.
+static thread_local cudaEvent_t *t_ev = nullptr;
+static thread_local int t_nev = 0, t_iev = 0;
+static inline void mark(cudaStream_t st) {
+  if (t_ev && t_iev < t_nev) cudaEventRecord(t_ev[t_iev++], st);
+}
+
 static int fail(int code, const std::string &msg) {
   g_err = msg;
   return code;
@@ -42,12 +49,16 @@ static int num_sms() {
   return sms;
 }
 
-// ----- tuning (per key width) ---------------------------------------------
-constexpr int SC_BLOCK = 512;
-constexpr int LC_BLOCK = 512;
-constexpr int LC_KPT = 16;
-constexpr int HI_BLOCK = 512;
-template <typename K> constexpr int sc_kpt() { return sizeof(K) == 4 ? 16 : 8; }
+// ----- tuning (per record width) --------------------------------------------
+// Scatter tiles and local-sort capacity by record bytes (key + value):
+//   4 B  (u32 keys):           tile 512x16 = 8192, local 512x16 = 8192
+//   8+ B (u64 keys, KV):       tile 256x16 = 4096, local 512x16 = 8192
+struct Tune {
+  int sc_block, sc_kpt, lc_block, lc_kpt;
+};
+constexpr Tune tune_for(int kb, int vb) {
+  return (kb + vb) <= 4 ? Tune{512, 16, 512, 16} : Tune{256, 16, 512, 16};
+}
 
 struct Geometry {
   uint64_t n;
@@ -62,8 +73,9 @@ static Geometry geometry(uint64_t n, int kb, int vb, int width_eff) {
   g.n = n;
   g.kb = kb;
   g.vb = vb;
-  g.tile = uint32_t(SC_BLOCK * (kb == 4 ? 16 : 8));
-  g.local_max = uint32_t(LC_BLOCK * LC_KPT);
+  const Tune tn = tune_for(kb, vb);
+  g.tile = uint32_t(tn.sc_block * tn.sc_kpt);
+  g.local_max = uint32_t(tn.lc_block * tn.lc_kpt);
   g.group_min = g.local_max / 8;
   g.ndig = (width_eff + 7) / 8;
   const uint64_t maxb = n / (uint64_t(g.local_max) + 1) + 2;
@@ -147,12 +159,14 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   ws.ndig = geo.ndig;
   ws.shift0 = int(sizeof(K) * 8) - width_eff;
 
-  constexpr int SKPT = sc_kpt<K>();
+  constexpr Tune TN = tune_for(int(sizeof(K)), VB);
+  constexpr int SC_BLOCK = TN.sc_block, SKPT = TN.sc_kpt, LC_BLOCK = TN.lc_block, LC_KPT = TN.lc_kpt;
+  constexpr int HI_BLOCK = SC_BLOCK, HKPT = SKPT;  // histogram tiles == scatter tiles
   using SS = ScatterSmem<K, VB, KIND, SC_BLOCK, SKPT>;
   using LS = LocalSmem<K, VB, KIND, LC_BLOCK, LC_KPT>;
   auto sc = scatter_kernel<K, VB, KIND, SC_BLOCK, SKPT>;
   auto lc = local_kernel<K, VB, KIND, LC_BLOCK, LC_KPT>;
-  auto hk = hist_kernel<K, KIND, HI_BLOCK, SKPT * SC_BLOCK / HI_BLOCK>;
+  auto hk = hist_kernel<K, KIND, HI_BLOCK, HKPT>;
   static int sc_grid = 0, lc_grid = 0, hk_grid = 0;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -166,21 +180,28 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   });
   if (attr_err != cudaSuccess) return fail(BS_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
 
+  mark(st);
   BS_CUDA(cudaMemsetAsync(ws.ctl, 0, sizeof(Ctl), st));
   {
     const uint32_t ntiles = uint32_t((n + geo.tile - 1) / geo.tile);
     const int g = int(min64((ntiles + 255) / 256 + 1, 4096));
     init_kernel<K, KIND><<<g, 256, 0, st>>>(ws);
   }
+  mark(st);
   if (n > geo.local_max) {
     const int nlev = geo.ndig + 1;
     for (int L = 0; L < nlev; ++L) {
-      hist_kernel<K, KIND, HI_BLOCK, SKPT * SC_BLOCK / HI_BLOCK><<<hk_grid, HI_BLOCK, 0, st>>>(ws, L);
+      hk<<<hk_grid, HI_BLOCK, 0, st>>>(ws, L);
+      mark(st);
       plan_kernel<K><<<num_sms() * 4, 256, 0, st>>>(ws, L);
+      expand_kernel<<<num_sms() * 4, 256, 0, st>>>(ws, L + 1);
+      mark(st);
       sc<<<sc_grid, SC_BLOCK, SS::bytes, st>>>(ws, L);
+      mark(st);
     }
   }
   lc<<<lc_grid, LC_BLOCK, LS::bytes, st>>>(ws);
+  mark(st);
   BS_CUDA(cudaGetLastError());
   return BS_OK;
 }
@@ -259,6 +280,41 @@ int bs_sort(void *keys, void *vals, uint64_t n, int key_bytes, int val_bytes, in
   if (rc) return rc;
   if (counters) return bs_metrics(keys, n, key_bytes, width, start_pos, key_kind, depth, nullptr, 0, stream, counters);
   return BS_OK;
+}
+
+int bs_sort_profiled(void *keys, void *vals, uint64_t n, int key_bytes, int val_bytes, int width, int start_pos,
+                     int key_kind, void *ws, size_t ws_bytes, void *stream, int64_t *counters, int64_t depth,
+                     float *phase_ms, int nphases, int *nrecorded) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int nev = nphases + 1;
+  cudaEvent_t evs[64];
+  if (nev > 64 || nphases < 1) return fail(BS_ERR_VALUE, "nphases must be in [1, 63]");
+  for (int i = 0; i < nev; ++i) BS_CUDA(cudaEventCreate(&evs[i]));
+  t_ev = evs;
+  t_nev = nev;
+  t_iev = 0;
+  const int rc = bs_sort(keys, vals, n, key_bytes, val_bytes, width, start_pos, key_kind, ws, ws_bytes, stream,
+                         counters, depth);
+  const int rec = t_iev;
+  t_ev = nullptr;
+  t_nev = t_iev = 0;
+  if (rc == BS_OK) {
+    BS_CUDA(cudaStreamSynchronize(st));
+    for (int i = 0; i + 1 < rec; ++i) BS_CUDA(cudaEventElapsedTime(&phase_ms[i], evs[i], evs[i + 1]));
+  }
+  for (int i = 0; i < nev; ++i) cudaEventDestroy(evs[i]);
+  if (nrecorded) *nrecorded = rec > 0 ? rec - 1 : 0;
+  return rc;
+}
+
+int bs_sort_launches(uint64_t n, int key_bytes, int width, int start_pos, int with_counters) {
+  const int width_eff = width - start_pos;
+  if (n <= 1 || width_eff <= 0) return 0;
+  const Geometry g = geometry(n, key_bytes, 0, width_eff);
+  int k = 2;  // init + local
+  if (n > g.local_max) k += 4 * (g.ndig + 1);
+  if (with_counters) k += 2;
+  return k;
 }
 
 size_t bs_metrics_workspace_bytes(uint64_t) { return 0; }

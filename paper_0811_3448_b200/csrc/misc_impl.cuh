@@ -206,15 +206,18 @@ __global__ void sample_kernel(const K *keys, uint64_t n, int shift0, uint64_t co
 }
 
 // class of a normalised key against R-1 sorted normalised splitters:
-// 2j (strictly between s_{j-1} and s_j) or 2j+1 (equal to s_j)
+// 2*#{s_j < key} + [key equals some s_j].  Class 2j holds keys strictly
+// between s_{j-1} and s_j, class 2j+1 keys equal to s_j; with duplicate
+// splitters a tied key takes the class of the first equal splitter.
 template <typename K>
 __device__ __forceinline__ uint32_t split_class(K nk, const K *spl, int nsp) {
-  uint32_t c = 0;
+  uint32_t lt = 0, eq = 0;
   for (int j = 0; j < nsp; ++j) {
     const K s = spl[j];
-    c += (nk > s) ? 2u : (nk == s ? 1u : 0u);
+    lt += (s < nk) ? 1u : 0u;
+    eq |= (s == nk) ? 1u : 0u;
   }
-  return c;
+  return 2u * lt + eq;
 }
 
 constexpr int SPLIT_BLOCK = 256;

@@ -224,7 +224,10 @@ __global__ void __launch_bounds__(BLOCK) hist_kernel(Ws ws, int L) {
 }
 
 // ---------------------------------------------------------------------------
-// plan: one CTA (256 threads) per bucket of level L.
+// plan: one CTA (256 threads) per bucket of level L.  Decides skip / requeue /
+// scatter, turns the histogram into digit bases in place, and emits the
+// children: large ones to the next level's list (their tiles are mapped by
+// expand_kernel), the rest to the local-sort task list.
 // ---------------------------------------------------------------------------
 struct Emit {
   uint64_t start;
@@ -248,6 +251,18 @@ __device__ __forceinline__ void emit_tasks(const Ws &ws, uint64_t start, uint64_
   }
 }
 
+__device__ __forceinline__ void push_bucket(const Ws &ws, int L, uint64_t start, uint32_t count,
+                                            uint32_t digit, uint32_t parity) {
+  const uint32_t slot = atomicAdd(&ws.ctl->nbuckets[L + 1], 1u);
+  const uint32_t nt = uint32_t((count + ws.tile - 1) / ws.tile);
+  const uint32_t t0 = atomicAdd(&ws.ctl->ntiles[L + 1], nt);
+  if (slot >= ws.maxb || t0 + nt > ws.maxtiles) {
+    atomicOr(&ws.ctl->error, 3u);
+    return;
+  }
+  ws.buckets[(L + 1) & 1][slot] = Bucket{start, count, t0, digit, parity, ACT_SCATTER, 0};
+}
+
 template <typename K>
 __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
   constexpr int W = KeyTraits<K>::BITS;
@@ -255,12 +270,11 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
   __shared__ uint32_t s_scan[16];
   __shared__ Emit s_emit[520];
   __shared__ uint32_t s_nemit;
-  __shared__ uint32_t s_slot[520];
   const int tid = threadIdx.x;
-  const int cur = L & 1, nxt = cur ^ 1;
-  const uint32_t nb = ws.ctl->nbuckets[L];
+  const int cur = L & 1;
+  const uint32_t nb = min(ws.ctl->nbuckets[L], ws.maxb);
   for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {
-    Bucket bk = ws.buckets[cur][b];
+    const Bucket bk = ws.buckets[cur][b];
     uint32_t *hist = ws.bhist[cur] + size_t(b) * 256;
     const uint32_t c = hist[tid];
     const K var = K(ws.bor[cur][b] ^ ws.band[cur][b]);
@@ -276,33 +290,9 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
     if (dstar != dig) {  // digit constant here (pass-through): requeue at dstar
       if (tid == 0) {
         ws.buckets[cur][b].action = ACT_SKIP;
-        if (bk.count <= ws.local_max) {
-          emit_tasks(ws, bk.start, bk.count, bk.parity);
-        } else {
-          const uint32_t slot = atomicAdd(&ws.ctl->nbuckets[L + 1], 1u);
-          const uint32_t nt = uint32_t((bk.count + ws.tile - 1) / ws.tile);
-          const uint32_t t0 = atomicAdd(&ws.ctl->ntiles[L + 1], nt);
-          if (slot >= ws.maxb || t0 + nt > ws.maxtiles) {
-            atomicOr(&ws.ctl->error, 3u);
-          } else {
-            ws.buckets[nxt][slot] = Bucket{bk.start, bk.count, t0, uint32_t(dstar), bk.parity, ACT_SCATTER, 0};
-            ws.bor[nxt][slot] = 0;
-            ws.band[nxt][slot] = ~uint64_t(0);
-            s_slot[0] = slot;
-            s_emit[0] = Emit{bk.start, bk.count, t0};
-          }
-        }
+        if (bk.count <= ws.local_max) emit_tasks(ws, bk.start, bk.count, bk.parity);
+        else push_bucket(ws, L, bk.start, bk.count, uint32_t(dstar), bk.parity);
       }
-      __syncthreads();
-      // requeued bucket: zero its histogram row and map its tiles (whole CTA)
-      if (bk.count > ws.local_max && !(ws.ctl->error & 3u)) {
-        const uint32_t slot = s_slot[0];
-        const uint32_t t0 = s_emit[0].kind;
-        const uint32_t nt = uint32_t((bk.count + ws.tile - 1) / ws.tile);
-        ws.bhist[nxt][size_t(slot) * 256 + tid] = 0;
-        for (uint32_t i = tid; i < nt; i += 256) ws.tile_bucket[nxt][t0 + i] = slot;
-      }
-      __syncthreads();
       continue;
     }
     // scatter this bucket on digit `dig`
@@ -329,7 +319,7 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
       for (int d = 0; d < 256; ++d) {
         const uint32_t cd = s_cnt[d];
         if (cd == 0) continue;
-        if (cd > ws.local_max || cd >= ws.group_min) {
+        if (cd >= ws.group_min) {
           if (gc) s_emit[ne++] = Emit{gs, gc, 1};
           gc = 0;
           s_emit[ne++] = Emit{pos, cd, cd > ws.local_max ? 0u : 1u};
@@ -351,51 +341,127 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
     for (uint32_t i = tid; i < ne; i += 256) {
       const Emit e = s_emit[i];
       if (e.kind == 1) {
-        // a singleton already home needs nothing
-        if (!(e.count == 1 && cpar == 0)) emit_tasks(ws, e.start, e.count, cpar);
-        s_slot[i] = 0xFFFFFFFFu;
+        if (!(e.count == 1 && cpar == 0)) emit_tasks(ws, e.start, e.count, cpar);  // singleton home: done
       } else {
-        const uint32_t slot = atomicAdd(&ws.ctl->nbuckets[L + 1], 1u);
-        const uint32_t nt = uint32_t((e.count + ws.tile - 1) / ws.tile);
-        const uint32_t t0 = atomicAdd(&ws.ctl->ntiles[L + 1], nt);
-        if (slot >= ws.maxb || t0 + nt > ws.maxtiles) {
-          atomicOr(&ws.ctl->error, 3u);
-          s_slot[i] = 0xFFFFFFFFu;
-        } else {
-          ws.buckets[nxt][slot] = Bucket{e.start, e.count, t0, uint32_t(dig + 1), cpar, ACT_SCATTER, 0};
-          ws.bor[nxt][slot] = 0;
-          ws.band[nxt][slot] = ~uint64_t(0);
-          s_slot[i] = slot;
-          s_emit[i].kind = 2u + t0;  // remember tile0 (kind >= 2 marks "large")
-        }
+        push_bucket(ws, L, e.start, e.count, uint32_t(dig + 1), cpar);
       }
-    }
-    __syncthreads();
-    for (uint32_t i = 0; i < ne; ++i) {
-      const uint32_t slot = s_slot[i];
-      if (slot == 0xFFFFFFFFu) continue;
-      const Emit e = s_emit[i];
-      const uint32_t t0 = e.kind - 2u;
-      const uint32_t nt = uint32_t((e.count + ws.tile - 1) / ws.tile);
-      ws.bhist[nxt][size_t(slot) * 256 + tid] = 0;
-      for (uint32_t k = tid; k < nt; k += 256) ws.tile_bucket[nxt][t0 + k] = slot;
     }
     __syncthreads();
   }
 }
 
+// expand: for every bucket of level L, clear its histogram row / masks and
+// map its tiles (tile -> bucket).  One warp per bucket.
+__global__ void __launch_bounds__(256) expand_kernel(Ws ws, int L) {
+  const int cur = L & 1;
+  const uint32_t nb = min(ws.ctl->nbuckets[L], ws.maxb);
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t b = gw; b < nb; b += nw) {
+    const Bucket bk = ws.buckets[cur][b];
+    uint4 *row = reinterpret_cast<uint4 *>(ws.bhist[cur] + size_t(b) * 256);
+    for (int i = lane; i < 64; i += 32) row[i] = make_uint4(0, 0, 0, 0);
+    if (lane == 0) {
+      ws.bor[cur][b] = 0;
+      ws.band[cur][b] = ~uint64_t(0);
+    }
+    const uint32_t nt = uint32_t((bk.count + ws.tile - 1) / ws.tile);
+    for (uint32_t i = lane; i < nt; i += 32) ws.tile_bucket[cur][bk.tile0 + i] = b;
+  }
+}
+
 // ---------------------------------------------------------------------------
-// K2+K3: stable scatter of one digit with single-pass decoupled look-back.
+// Block ranking.  STABLE: warp-private counters + ballot match (ties keep
+// element order; element (w, j, lane) <-> w*32*k + 32*j + lane).  Otherwise
+// one block-shared counter per digit and shared-memory atomics (keys-only
+// passes whose tie order is immaterial: the MSD scatter and the first LSD
+// pass of the local sort).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t match_digit8_ptx(uint32_t d, uint32_t active) {
+  uint32_t peers = active;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    uint32_t bb;
+    asm volatile(
+        "{\n .reg .pred p;\n .reg .u32 t;\n and.b32 t, %1, %2;\n setp.ne.u32 p, t, 0;\n"
+        " vote.sync.ballot.b32 %0, p, 0xffffffff;\n @!p not.b32 %0, %0;\n}\n"
+        : "=r"(bb)
+        : "r"(d), "r"(1u << b));
+    peers &= bb;
+  }
+  return peers;
+}
+
+// Ranks (< 65536) of KPT elements packed two per register.
+template <int KPT>
+struct Ranks {
+  uint32_t r[(KPT + 1) / 2];
+  __device__ __forceinline__ void clear() {
+#pragma unroll
+    for (int i = 0; i < (KPT + 1) / 2; ++i) r[i] = 0;
+  }
+  __device__ __forceinline__ void set(int j, uint32_t v) { r[j >> 1] |= v << (16 * (j & 1)); }
+  __device__ __forceinline__ uint32_t get(int j) const { return (r[j >> 1] >> (16 * (j & 1))) & 0xFFFFu; }
+};
+
+// Stable warp ranking of the first `kk` (warp-uniform) chunks.
+template <int KPT>
+__device__ __forceinline__ void warp_rank_stable(const uint32_t (&dig)[KPT], int kk, int nvalid,
+                                                 uint32_t *whist, Ranks<KPT> &rank) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) {
+    if (j >= kk || 32 * j >= nvalid) break;
+    const bool valid = 32 * j + lane < nvalid;
+    const uint32_t active = __ballot_sync(0xFFFFFFFFu, valid);
+    const uint32_t d = dig[j];
+    const uint32_t peers = match_digit8_ptx(d, active);
+    const uint32_t below = __popc(peers & lt);
+    uint32_t old = 0;
+    if (valid && below == 0) {
+      old = whist[d];
+      whist[d] = old + __popc(peers);
+    }
+    old = __shfl_sync(0xFFFFFFFFu, old, valid ? (__ffs(peers) - 1) : lane);
+    rank.set(j, valid ? old + below : 0u);
+    __syncwarp();
+  }
+}
+
+// After ranking: per digit, prefix over warps (stable) -> whist[w][d] holds
+// the exclusive warp prefix; returns the tile total of digit `tid` (< 256).
+template <int NW>
+__device__ __forceinline__ uint32_t warp_prefix(uint32_t *whist_all) {
+  const int tid = threadIdx.x;
+  uint32_t s = 0;
+  if (tid < 256) {
+    uint32_t c[NW];
+#pragma unroll
+    for (int ww = 0; ww < NW; ++ww) c[ww] = whist_all[ww * 256 + tid];
+#pragma unroll
+    for (int ww = 0; ww < NW; ++ww) {
+      whist_all[ww * 256 + tid] = s;
+      s += c[ww];
+    }
+  }
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// K2+K3: scatter one digit with single-pass decoupled look-back.
 // ---------------------------------------------------------------------------
 template <typename K, int VB, int KIND, int BLOCK, int KPT>
 struct ScatterSmem {
   using V = typename ValT<VB>::T;
+  static constexpr bool STABLE = VB != 0;
   static constexpr int TILE = BLOCK * KPT;
   static constexpr int NW = BLOCK / 32;
   static constexpr size_t keys_off = 0;
   static constexpr size_t vals_off = keys_off + sizeof(K) * TILE;
   static constexpr size_t whist_off = vals_off + (VB ? sizeof(V) * TILE : 0);
-  static constexpr size_t gbase_off = whist_off + sizeof(uint32_t) * NW * 256;
+  static constexpr size_t gbase_off = whist_off + sizeof(uint32_t) * (STABLE ? NW : 1) * 256;
   static constexpr size_t tstart_off = gbase_off + sizeof(uint64_t) * 256;
   static constexpr size_t misc_off = tstart_off + sizeof(uint32_t) * 256;
   static constexpr size_t bytes = misc_off + sizeof(uint32_t) * 32;
@@ -405,6 +471,7 @@ template <typename K, int VB, int KIND, int BLOCK, int KPT>
 __global__ void __launch_bounds__(BLOCK) scatter_kernel(Ws ws, int L) {
   using S = ScatterSmem<K, VB, KIND, BLOCK, KPT>;
   using V = typename S::V;
+  constexpr bool STABLE = S::STABLE;
   constexpr int TILE = S::TILE;
   extern __shared__ __align__(16) unsigned char smem[];
   K *keys_s = reinterpret_cast<K *>(smem + S::keys_off);
@@ -418,11 +485,15 @@ __global__ void __launch_bounds__(BLOCK) scatter_kernel(Ws ws, int L) {
   const uint32_t nt = ws.ctl->ntiles[L];
   if (nt == 0) return;
   const KeyGeom<K, KIND> g{ws.shift0};
-  uint32_t *whist = whist_all + w * 256;
+  uint32_t *whist = STABLE ? whist_all + w * 256 : whist_all;
   for (;;) {
     if (tid == 0) misc[16] = atomicAdd(&ws.ctl->ticket[L], 1u);
+    if constexpr (STABLE) {
 #pragma unroll
-    for (int i = lane; i < 256; i += 32) whist[i] = 0;
+      for (int i = lane; i < 256; i += 32) whist[i] = 0;
+    } else {
+      if (tid < 256) whist[tid] = 0;
+    }
     __syncthreads();
     const uint32_t t = misc[16];
     if (t >= nt) break;
@@ -434,39 +505,42 @@ __global__ void __launch_bounds__(BLOCK) scatter_kernel(Ws ws, int L) {
     }
     const uint32_t tin = t - bk.tile0;
     const uint64_t off = uint64_t(tin) * TILE;
-    const uint32_t cnt = uint32_t(min64(TILE, bk.count - off));
+    const int cnt = int(min64(TILE, bk.count - off));
     const K *src = static_cast<const K *>(ws.keys[bk.parity]) + bk.start + off;
     K *dst = static_cast<K *>(ws.keys[bk.parity ^ 1]);
     const V *vsrc = VB ? static_cast<const V *>(ws.vals[bk.parity]) + bk.start + off : nullptr;
     V *vdst = VB ? static_cast<V *>(ws.vals[bk.parity ^ 1]) : nullptr;
     const int dig = int(bk.digit);
     const int wbase = w * 32 * KPT;
-    const int nvw = max(0, min(32 * KPT, int(cnt) - wbase));
     K x[KPT];
     V v[KPT];
-    uint32_t dg[KPT], rk[KPT];
+    Ranks<KPT> rk;
+    rk.clear();
 #pragma unroll
     for (int j = 0; j < KPT; ++j) {
       const int e = wbase + 32 * j + lane;
-      if (e < int(cnt)) {
+      x[j] = 0;
+      if (e < cnt) {
         x[j] = __ldcs(src + e);
         if constexpr (VB != 0) v[j] = __ldcs(vsrc + e);
       }
     }
+    if constexpr (STABLE) {
+      uint32_t dg[KPT];
 #pragma unroll
-    for (int j = 0; j < KPT; ++j) dg[j] = g.digit(x[j], dig);
-    warp_rank<KPT>(dg, nvw, whist, rk);
-    __syncthreads();
-    uint32_t total = 0;
-    if (tid < 256) {
-      uint32_t s = 0;
-      for (int ww = 0; ww < S::NW; ++ww) {
-        const uint32_t cc = whist_all[ww * 256 + tid];
-        whist_all[ww * 256 + tid] = s;
-        s += cc;
+      for (int j = 0; j < KPT; ++j) dg[j] = g.digit(x[j], dig);
+      warp_rank_stable<KPT>(dg, KPT, max(0, min(32 * KPT, cnt - wbase)), whist, rk);
+    } else {
+#pragma unroll
+      for (int j = 0; j < KPT; ++j) {
+        const int e = wbase + 32 * j + lane;
+        if (e < cnt) rk.set(j, atomicAdd(&whist[g.digit(x[j], dig)], 1u));
       }
-      total = s;
     }
+    __syncthreads();
+    uint32_t total;
+    if constexpr (STABLE) total = warp_prefix<S::NW>(whist_all);
+    else total = (tid < 256) ? whist[tid] : 0u;
     const uint32_t texcl = scan256_excl<BLOCK>(total, misc);
     if (tid < 256) {
       tstart[tid] = texcl;
@@ -493,16 +567,17 @@ __global__ void __launch_bounds__(BLOCK) scatter_kernel(Ws ws, int L) {
 #pragma unroll
     for (int j = 0; j < KPT; ++j) {
       const int e = wbase + 32 * j + lane;
-      if (e < int(cnt)) {
-        const uint32_t d = dg[j];
-        const uint32_t pos = tstart[d] + whist[d] + rk[j];
+      if (e < cnt) {
+        const uint32_t d = g.digit(x[j], dig);
+        uint32_t pos = tstart[d] + rk.get(j);
+        if constexpr (STABLE) pos += whist[d];
         keys_s[pos] = x[j];
         if constexpr (VB != 0) vals_s[pos] = v[j];
       }
     }
     __syncthreads();
 #pragma unroll 4
-    for (int e = tid; e < int(cnt); e += BLOCK) {
+    for (int e = tid; e < cnt; e += BLOCK) {
       const K k = keys_s[e];
       const uint64_t o = gbase[g.digit(k, dig)] + uint64_t(e);
       __stcs(dst + o, k);
@@ -514,9 +589,12 @@ __global__ void __launch_bounds__(BLOCK) scatter_kernel(Ws ws, int L) {
 
 // ---------------------------------------------------------------------------
 // K4: local sort of one task (<= BLOCK*KPT elements) per CTA iteration.  LSD
-// over the task's varying digits only (all-equal digits are the reference's
-// pass-throughs), stable, keys (+values) staged through shared memory, final
-// pass written to the caller's buffer.
+// over the task's varying digits only (constant digits are the reference's
+// pass-throughs), keys (+values) held in registers with k = ceil(n/BLOCK)
+// elements per thread, staged through one shared buffer per pass; the final
+// pass is written coalesced to the caller's buffer.  Keys-only tasks rank the
+// first pass with shared atomics (its tie order is immaterial), later passes
+// (and every pass with values) with the stable ballot ranking.
 // ---------------------------------------------------------------------------
 template <typename K, int VB, int KIND, int BLOCK, int KPT>
 struct LocalSmem {
@@ -548,24 +626,27 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
   const uint32_t ntasks = min(ws.ctl->ntasks, ws.maxtasks);
   const KeyGeom<K, KIND> g{ws.shift0};
   uint32_t *whist = whist_all + w * 256;
-  const int wbase = w * 32 * KPT;
   for (uint32_t ti = blockIdx.x; ti < ntasks; ti += gridDim.x) {
     const Task tk = ws.tasks[ti];
     const int n = int(tk.count);
+    const int kk = (n + BLOCK - 1) / BLOCK;  // elements per thread for this task
+    const int wbase = w * 32 * kk;
+    const int nvw = max(0, min(32 * kk, n - wbase));
     const K *src = static_cast<const K *>(ws.keys[tk.parity]) + tk.start;
     K *dst = static_cast<K *>(ws.keys[0]) + tk.start;
     const V *vsrc = VB ? static_cast<const V *>(ws.vals[tk.parity]) + tk.start : nullptr;
     V *vdst = VB ? static_cast<V *>(ws.vals[0]) + tk.start : nullptr;
-    const int nvw = max(0, min(32 * KPT, n - wbase));
     K x[KPT];
     V v[KPT];
     K o = 0, a = ~K(0);
 #pragma unroll
     for (int j = 0; j < KPT; ++j) {
+      if (j >= kk) break;
       const int e = wbase + 32 * j + lane;
-      if (e < n) {
-        x[j] = src[e];
-        if constexpr (VB != 0) v[j] = vsrc[e];
+      x[j] = 0;
+      if (32 * j + lane < nvw) {
+        x[j] = __ldcs(src + e);
+        if constexpr (VB != 0) v[j] = __ldcs(vsrc + e);
         const K nk = g.norm(x[j]);
         o |= nk;
         a &= nk;
@@ -592,8 +673,9 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
       if (tk.parity) {
 #pragma unroll
         for (int j = 0; j < KPT; ++j) {
+          if (j >= kk) break;
           const int e = wbase + 32 * j + lane;
-          if (e < n) {
+          if (32 * j + lane < nvw) {
             dst[e] = x[j];
             if constexpr (VB != 0) vdst[e] = v[j];
           }
@@ -605,58 +687,63 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
     // digits that vary, least significant first
     const int lastd = (W - 1 - (__ffsll((long long)(uint64_t(var))) - 1)) >> 3;
     const int firstd = KeyTraits<K>::clz(var) >> 3;
-    bool wrote_smem = false;
+    bool first = true;
     for (int dig = lastd; dig >= firstd; --dig) {
       if (((var >> (W - 8 - 8 * dig)) & K(0xFF)) == 0) continue;
-      if (wrote_smem) {
+      if (!first) {
         // reload in element order from the previous pass
 #pragma unroll
         for (int j = 0; j < KPT; ++j) {
+          if (j >= kk) break;
           const int e = wbase + 32 * j + lane;
-          if (e < n) {
+          if (32 * j + lane < nvw) {
             x[j] = keys_s[e];
             if constexpr (VB != 0) v[j] = vals_s[e];
           }
         }
         __syncthreads();
       }
+      const bool atomic_pass = (VB == 0) && first;
+      Ranks<KPT> rk;
+      rk.clear();
+      if (atomic_pass) {
+        if (tid < 256) whist_all[tid] = 0;
+        __syncthreads();
 #pragma unroll
-      for (int i = lane; i < 256; i += 32) whist[i] = 0;
-      __syncwarp();
-      uint32_t dg[KPT], rk[KPT];
-#pragma unroll
-      for (int j = 0; j < KPT; ++j) dg[j] = g.digit(x[j], dig);
-      warp_rank<KPT>(dg, nvw, whist, rk);
-      __syncthreads();
-      uint32_t total = 0;
-      if (tid < 256) {
-        uint32_t s = 0;
-        for (int ww = 0; ww < S::NW; ++ww) {
-          const uint32_t cc = whist_all[ww * 256 + tid];
-          whist_all[ww * 256 + tid] = s;
-          s += cc;
+        for (int j = 0; j < KPT; ++j) {
+          if (j >= kk) break;
+          if (32 * j + lane < nvw) rk.set(j, atomicAdd(&whist_all[g.digit(x[j], dig)], 1u));
         }
-        total = s;
+      } else {
+#pragma unroll
+        for (int i = lane; i < 256; i += 32) whist[i] = 0;
+        __syncwarp();
+        uint32_t dg[KPT];
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) dg[j] = (j < kk) ? g.digit(x[j], dig) : 0u;
+        warp_rank_stable<KPT>(dg, kk, nvw, whist, rk);
       }
+      __syncthreads();
+      const uint32_t total = atomic_pass ? ((tid < 256) ? whist_all[tid] : 0u) : warp_prefix<S::NW>(whist_all);
       const uint32_t texcl = scan256_excl<BLOCK>(total, misc);
       if (tid < 256) tstart[tid] = texcl;
       __syncthreads();
 #pragma unroll
       for (int j = 0; j < KPT; ++j) {
-        const int e = wbase + 32 * j + lane;
-        if (e < n) {
-          const uint32_t d = dg[j];
-          const uint32_t pos = tstart[d] + whist[d] + rk[j];
+        if (j >= kk) break;
+        if (32 * j + lane < nvw) {
+          const uint32_t d = g.digit(x[j], dig);
+          const uint32_t pos = tstart[d] + rk.get(j) + (atomic_pass ? 0u : whist[d]);
           keys_s[pos] = x[j];
           if constexpr (VB != 0) vals_s[pos] = v[j];
         }
       }
       __syncthreads();
-      wrote_smem = true;
+      first = false;
     }
     for (int e = tid; e < n; e += BLOCK) {
-      dst[e] = keys_s[e];
-      if constexpr (VB != 0) vdst[e] = vals_s[e];
+      __stcs(dst + e, keys_s[e]);
+      if constexpr (VB != 0) __stcs(vdst + e, vals_s[e]);
     }
     __syncthreads();
   }
