@@ -178,3 +178,66 @@ __device__ __forceinline__ T warp_and(T v) {
 }
 
 }  // namespace bs
+
+// ---------------------------------------------------------------------------
+// TMA bulk copies (cp.async.bulk, SASS UBLKCP) global -> shared, completed on
+// an mbarrier.  Used to double-buffer tiles/tasks so the next one streams in
+// while the current one is ranked and scattered.
+// ---------------------------------------------------------------------------
+namespace bs {
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// order earlier generic-proxy accesses of shared memory before async-proxy ones
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Span of elements [0, cnt) of `src` widened to the enclosing 16-byte aligned
+// granules (an over-read that stays inside granules holding valid elements,
+// so it never crosses a page).  `head` = element offset of src[0] in it.
+struct Span {
+  const void *base;
+  uint32_t bytes;
+  uint32_t head;
+};
+template <typename T>
+__device__ __forceinline__ Span span16(const T *src, uint32_t cnt) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+  const uintptr_t a0 = a & ~uintptr_t(15);
+  const uintptr_t a1 = (a + uintptr_t(cnt) * sizeof(T) + 15) & ~uintptr_t(15);
+  return Span{reinterpret_cast<const void *>(a0), uint32_t(a1 - a0), uint32_t((a - a0) / sizeof(T))};
+}
+
+}  // namespace bs

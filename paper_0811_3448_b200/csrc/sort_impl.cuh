@@ -449,45 +449,194 @@ __device__ __forceinline__ uint32_t warp_prefix(uint32_t *whist_all) {
   return s;
 }
 
+// Decoupled look-back for digit `d` of tile `t` (t > tile0): sum the
+// predecessors' counts back to the nearest inclusive prefix.  Statuses are
+// read 8 tiles at a time so one walk step costs one L2 round trip per 8
+// predecessors instead of one per predecessor.
+__device__ __forceinline__ uint32_t lookback(const uint32_t *status, uint32_t t, uint32_t tile0, int d) {
+  constexpr int WIN = 8;
+  uint32_t prefix = 0;
+  uint32_t p = t - 1;  // p >= tile0
+  for (;;) {
+    const int n = int(min(uint32_t(WIN), p - tile0 + 1));
+    uint32_t sv[WIN];
+#pragma unroll
+    for (int i = 0; i < WIN; ++i) sv[i] = (i < n) ? ld_relaxed(status + size_t(p - i) * 256 + d) : 0u;
+    int i = 0;
+    for (; i < n; ++i) {
+      const uint32_t f = sv[i] & ~ST_MASK;
+      if (f == 0) break;  // not published yet: re-poll from here
+      prefix += sv[i] & ST_MASK;
+      if (f == ST_INCL) return prefix;
+    }
+    p -= uint32_t(i);
+  }
+}
+
 // ---------------------------------------------------------------------------
-// K2+K3: scatter one digit with single-pass decoupled look-back.
+// Block-wide exclusive scan of one value per thread (any BLOCK <= 1024).
+// ---------------------------------------------------------------------------
+template <int BLOCK>
+__device__ __forceinline__ uint32_t block_scan_excl(uint32_t x, uint32_t *scratch /* >= 33 words */) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  uint32_t incl = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) scratch[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    const uint32_t s = (lane < BLOCK / 32) ? scratch[lane] : 0u;
+    uint32_t si = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, si, o);
+      if (lane >= o) si += y;
+    }
+    if (lane < BLOCK / 32) scratch[lane] = si - s;
+  }
+  __syncthreads();
+  const uint32_t r = scratch[w] + incl - x;
+  __syncthreads();
+  return r;
+}
+
+// Inverse of KeyGeom::norm for shift0 == 0 (raw word from its encoded key).
+template <typename K, int KIND>
+__device__ __forceinline__ K denorm(K nk) {
+  constexpr K MSB = K(1) << (KeyTraits<K>::BITS - 1);
+  if constexpr (KIND == 0) return nk;
+  else if constexpr (KIND == 1) return nk ^ MSB;
+  else return (nk & MSB) ? (nk ^ MSB) : ~nk;
+}
+
+// Double-buffered input: two (keys[, vals]) buffers filled by TMA bulk copies.
+template <typename K, int VB, int CAP>
+struct DBuf {
+  using V = typename ValT<VB>::T;
+  static constexpr size_t kbuf = (sizeof(K) * CAP + 32 + 15) & ~size_t(15);
+  static constexpr size_t vbuf = VB ? ((sizeof(V) * CAP + 32 + 15) & ~size_t(15)) : 0;
+  static constexpr size_t bytes = 2 * (kbuf + vbuf);
+  __device__ static K *keys(unsigned char *base, int i) { return reinterpret_cast<K *>(base + i * kbuf); }
+  __device__ static V *vals(unsigned char *base, int i) {
+    return reinterpret_cast<V *>(base + 2 * kbuf + i * vbuf);
+  }
+};
+
+struct InFlight {
+  uint64_t start;  // element offset of the range in the array
+  uint32_t idx;    // tile id / task id (>= limit: none)
+  uint32_t b;      // bucket (scatter)
+  uint32_t cnt;
+  uint32_t digit;
+  uint32_t parity;
+  uint32_t tin;
+  uint32_t tile0;
+  uint32_t headk, headv;
+  uint32_t valid;  // data copy issued
+};
+
+// Thread 0 only: issue the bulk copies of range [start, start+cnt) of the
+// parity-`par` buffers into slot `slot`.
+template <typename K, int VB, int CAP>
+__device__ __forceinline__ void issue_copy(const Ws &ws, unsigned char *dbuf, uint64_t *bars, int slot,
+                                           InFlight &f) {
+  using D = DBuf<K, VB, CAP>;
+  using V = typename D::V;
+  const K *src = static_cast<const K *>(ws.keys[f.parity]) + f.start;
+  const Span sk = span16(src, f.cnt);
+  Span sv{nullptr, 0, 0};
+  if constexpr (VB != 0) sv = span16(static_cast<const V *>(ws.vals[f.parity]) + f.start, f.cnt);
+  f.headk = sk.head;
+  f.headv = sv.head;
+  fence_proxy_async_smem();
+  mbar_arrive_expect_tx(&bars[slot], sk.bytes + sv.bytes);
+  bulk_g2s(D::keys(dbuf, slot), sk.base, sk.bytes, &bars[slot]);
+  if constexpr (VB != 0) bulk_g2s(D::vals(dbuf, slot), sv.base, sv.bytes, &bars[slot]);
+}
+
+// ---------------------------------------------------------------------------
+// K2+K3: scatter one digit with single-pass decoupled look-back.  Persistent
+// CTAs claim tiles in order; the next tile is bulk-copied (TMA) into the
+// spare buffer while the current one is ranked, scanned and scattered; the
+// consumed input buffer doubles as the staging buffer for the coalesced
+// write-out.
 // ---------------------------------------------------------------------------
 template <typename K, int VB, int KIND, int BLOCK, int KPT>
 struct ScatterSmem {
   using V = typename ValT<VB>::T;
+  using D = DBuf<K, VB, BLOCK * KPT>;
   static constexpr bool STABLE = VB != 0;
   static constexpr int TILE = BLOCK * KPT;
   static constexpr int NW = BLOCK / 32;
-  static constexpr size_t keys_off = 0;
-  static constexpr size_t vals_off = keys_off + sizeof(K) * TILE;
-  static constexpr size_t whist_off = vals_off + (VB ? sizeof(V) * TILE : 0);
+  static constexpr size_t dbuf_off = 0;
+  static constexpr size_t whist_off = dbuf_off + D::bytes;
   static constexpr size_t gbase_off = whist_off + sizeof(uint32_t) * (STABLE ? NW : 1) * 256;
   static constexpr size_t tstart_off = gbase_off + sizeof(uint64_t) * 256;
   static constexpr size_t misc_off = tstart_off + sizeof(uint32_t) * 256;
-  static constexpr size_t bytes = misc_off + sizeof(uint32_t) * 32;
+  static constexpr size_t bars_off = misc_off + sizeof(uint32_t) * 64;
+  static constexpr size_t info_off = bars_off + sizeof(uint64_t) * 2;
+  static constexpr size_t bytes = info_off + sizeof(InFlight) * 2;
 };
 
 template <typename K, int VB, int KIND, int BLOCK, int KPT>
 __global__ void __launch_bounds__(BLOCK) scatter_kernel(Ws ws, int L) {
   using S = ScatterSmem<K, VB, KIND, BLOCK, KPT>;
+  using D = typename S::D;
   using V = typename S::V;
   constexpr bool STABLE = S::STABLE;
   constexpr int TILE = S::TILE;
-  extern __shared__ __align__(16) unsigned char smem[];
-  K *keys_s = reinterpret_cast<K *>(smem + S::keys_off);
-  V *vals_s = reinterpret_cast<V *>(smem + S::vals_off);
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned char *dbuf = smem + S::dbuf_off;
   uint32_t *whist_all = reinterpret_cast<uint32_t *>(smem + S::whist_off);
   uint64_t *gbase = reinterpret_cast<uint64_t *>(smem + S::gbase_off);
   uint32_t *tstart = reinterpret_cast<uint32_t *>(smem + S::tstart_off);
   uint32_t *misc = reinterpret_cast<uint32_t *>(smem + S::misc_off);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + S::bars_off);
+  InFlight *info = reinterpret_cast<InFlight *>(smem + S::info_off);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int cur = L & 1;
+  const int lv = L & 1;
   const uint32_t nt = ws.ctl->ntiles[L];
   if (nt == 0) return;
   const KeyGeom<K, KIND> g{ws.shift0};
   uint32_t *whist = STABLE ? whist_all + w * 256 : whist_all;
+
+  // thread 0: claim the next tile and start its copy into `slot`
+  auto claim = [&](int slot) {
+    InFlight f{};
+    f.idx = atomicAdd(&ws.ctl->ticket[L], 1u);
+    f.valid = 0;
+    if (f.idx < nt) {
+      const uint32_t b = ws.tile_bucket[lv][f.idx];
+      const Bucket bk = ws.buckets[lv][b];
+      f.b = b;
+      f.tin = f.idx - bk.tile0;
+      f.tile0 = bk.tile0;
+      f.digit = bk.digit;
+      f.parity = bk.parity;
+      const uint64_t off = uint64_t(f.tin) * TILE;
+      f.start = bk.start + off;
+      f.cnt = uint32_t(min64(TILE, bk.count - off));
+      if (bk.action == ACT_SCATTER) {
+        f.valid = 1;
+        issue_copy<K, VB, TILE>(ws, dbuf, bars, slot, f);
+      }
+    }
+    info[slot] = f;
+  };
+
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+    claim(0);
+  }
+  uint32_t phase = 0;  // bit i: parity of buffer i's next completion
+  int cur = 0;
   for (;;) {
-    if (tid == 0) misc[16] = atomicAdd(&ws.ctl->ticket[L], 1u);
+    if (tid == 0) claim(cur ^ 1);  // spare buffer is free: previous tile fully consumed
     if constexpr (STABLE) {
 #pragma unroll
       for (int i = lane; i < 256; i += 32) whist[i] = 0;
@@ -495,22 +644,19 @@ __global__ void __launch_bounds__(BLOCK) scatter_kernel(Ws ws, int L) {
       if (tid < 256) whist[tid] = 0;
     }
     __syncthreads();
-    const uint32_t t = misc[16];
-    if (t >= nt) break;
-    const uint32_t b = ws.tile_bucket[cur][t];
-    const Bucket bk = ws.buckets[cur][b];
-    if (bk.action != ACT_SCATTER) {
+    const InFlight f = info[cur];
+    if (f.idx >= nt) break;
+    if (!f.valid) {
       __syncthreads();
+      cur ^= 1;
       continue;
     }
-    const uint32_t tin = t - bk.tile0;
-    const uint64_t off = uint64_t(tin) * TILE;
-    const int cnt = int(min64(TILE, bk.count - off));
-    const K *src = static_cast<const K *>(ws.keys[bk.parity]) + bk.start + off;
-    K *dst = static_cast<K *>(ws.keys[bk.parity ^ 1]);
-    const V *vsrc = VB ? static_cast<const V *>(ws.vals[bk.parity]) + bk.start + off : nullptr;
-    V *vdst = VB ? static_cast<V *>(ws.vals[bk.parity ^ 1]) : nullptr;
-    const int dig = int(bk.digit);
+    mbar_wait(&bars[cur], (phase >> cur) & 1u);
+    phase ^= 1u << cur;
+    K *kb = D::keys(dbuf, cur);
+    V *vbp = D::vals(dbuf, cur);
+    const int cnt = int(f.cnt);
+    const int dig = int(f.digit);
     const int wbase = w * 32 * KPT;
     K x[KPT];
     V v[KPT];
@@ -521,8 +667,8 @@ __global__ void __launch_bounds__(BLOCK) scatter_kernel(Ws ws, int L) {
       const int e = wbase + 32 * j + lane;
       x[j] = 0;
       if (e < cnt) {
-        x[j] = __ldcs(src + e);
-        if constexpr (VB != 0) v[j] = __ldcs(vsrc + e);
+        x[j] = kb[f.headk + e];
+        if constexpr (VB != 0) v[j] = vbp[f.headv + e];
       }
     }
     if constexpr (STABLE) {
@@ -541,29 +687,22 @@ __global__ void __launch_bounds__(BLOCK) scatter_kernel(Ws ws, int L) {
     uint32_t total;
     if constexpr (STABLE) total = warp_prefix<S::NW>(whist_all);
     else total = (tid < 256) ? whist[tid] : 0u;
+    // publish this tile's digit counts first so successors can look past it
+    uint32_t *st = ws.status + size_t(f.idx) * 256 + tid;
+    if (tid < 256) st_relaxed(st, (f.tin == 0 ? ST_INCL : ST_AGG) | total);
     const uint32_t texcl = scan256_excl<BLOCK>(total, misc);
     if (tid < 256) {
       tstart[tid] = texcl;
-      uint32_t *st = ws.status + size_t(t) * 256 + tid;
       uint32_t prefix = 0;
-      if (tin == 0) {
-        st_relaxed(st, ST_INCL | total);
-      } else {
-        st_relaxed(st, ST_AGG | total);
-        uint32_t p = t - 1;
-        for (;;) {
-          const uint32_t sv = ld_relaxed(ws.status + size_t(p) * 256 + tid);
-          const uint32_t f = sv & ~ST_MASK;
-          if (f == 0) continue;
-          prefix += sv & ST_MASK;
-          if (f == ST_INCL) break;
-          --p;
-        }
+      if (f.tin != 0) {
+        prefix = lookback(ws.status, f.idx, f.tile0, tid);
         st_relaxed(st, ST_INCL | (prefix + total));
       }
-      gbase[tid] = bk.start + uint64_t(ws.bhist[cur][size_t(b) * 256 + tid]) + prefix - texcl;
+      const uint64_t tile_bucket_start = f.start - uint64_t(f.tin) * TILE;
+      gbase[tid] = tile_bucket_start + uint64_t(ws.bhist[lv][size_t(f.b) * 256 + tid]) + prefix - texcl;
     }
     __syncthreads();
+    // stage in digit order (the input buffer is consumed: keys are in registers)
 #pragma unroll
     for (int j = 0; j < KPT; ++j) {
       const int e = wbase + 32 * j + lane;
@@ -571,71 +710,117 @@ __global__ void __launch_bounds__(BLOCK) scatter_kernel(Ws ws, int L) {
         const uint32_t d = g.digit(x[j], dig);
         uint32_t pos = tstart[d] + rk.get(j);
         if constexpr (STABLE) pos += whist[d];
-        keys_s[pos] = x[j];
-        if constexpr (VB != 0) vals_s[pos] = v[j];
+        kb[pos] = x[j];
+        if constexpr (VB != 0) vbp[pos] = v[j];
       }
     }
     __syncthreads();
+    K *dst = static_cast<K *>(ws.keys[f.parity ^ 1]);
+    V *vdst = VB ? static_cast<V *>(ws.vals[f.parity ^ 1]) : nullptr;
 #pragma unroll 4
     for (int e = tid; e < cnt; e += BLOCK) {
-      const K k = keys_s[e];
+      const K k = kb[e];
       const uint64_t o = gbase[g.digit(k, dig)] + uint64_t(e);
       __stcs(dst + o, k);
-      if constexpr (VB != 0) __stcs(vdst + o, vals_s[e]);
+      if constexpr (VB != 0) __stcs(vdst + o, vbp[e]);
     }
     __syncthreads();
+    cur ^= 1;
   }
 }
 
 // ---------------------------------------------------------------------------
-// K4: local sort of one task (<= BLOCK*KPT elements) per CTA iteration.  LSD
-// over the task's varying digits only (constant digits are the reference's
-// pass-throughs), keys (+values) held in registers with k = ceil(n/BLOCK)
-// elements per thread, staged through one shared buffer per pass; the final
-// pass is written coalesced to the caller's buffer.  Keys-only tasks rank the
-// first pass with shared atomics (its tie order is immaterial), later passes
-// (and every pass with values) with the stable ballot ranking.
+// K4: local sort of one task (<= BLOCK*KPT elements) per CTA iteration; the
+// next task streams in by TMA bulk copy while the current one is sorted.
+//  * Dense keys-only tasks (full-width words, all varying bits inside a
+//    16-bit span -- the common case after two 8-bit MSD levels): counting sort
+//    through a presence bitmap, one shared atomic per key, emitted in value
+//    order.
+//  * Otherwise LSD over the task's varying digits only (constant digits are
+//    the reference's pass-throughs), keys (+values) in registers, k =
+//    ceil(n/BLOCK) per thread; the first keys-only pass ranks with shared
+//    atomics, later passes (and all passes with values) with the stable
+//    ballot ranking.
+// The consumed input buffer is the staging buffer of every pass; the final
+// pass is written coalesced to the caller's buffer.
 // ---------------------------------------------------------------------------
 template <typename K, int VB, int KIND, int BLOCK, int KPT>
 struct LocalSmem {
   using V = typename ValT<VB>::T;
   static constexpr int CAP = BLOCK * KPT;
+  using D = DBuf<K, VB, CAP>;
   static constexpr int NW = BLOCK / 32;
-  static constexpr size_t keys_off = 0;
-  static constexpr size_t vals_off = keys_off + sizeof(K) * CAP;
-  static constexpr size_t whist_off = vals_off + (VB ? sizeof(V) * CAP : 0);
-  static constexpr size_t tstart_off = whist_off + sizeof(uint32_t) * NW * 256;
+  static constexpr int BM_WORDS = 2048;  // 2^16 values
+  static constexpr int OVF_CAP = 1024;
+  static constexpr size_t dbuf_off = 0;
+  static constexpr size_t whist_off = dbuf_off + D::bytes;
+  static constexpr size_t whist_bytes = sizeof(uint32_t) * NW * 256;
+  static constexpr size_t bm_bytes = VB ? 0 : sizeof(uint32_t) * (3 * BM_WORDS + OVF_CAP + 4);
+  static constexpr size_t tstart_off = whist_off + (whist_bytes > bm_bytes ? whist_bytes : bm_bytes);
   static constexpr size_t red_off = tstart_off + sizeof(uint32_t) * 256;
   static constexpr size_t misc_off = red_off + sizeof(uint64_t) * 2 * NW;
-  static constexpr size_t bytes = misc_off + sizeof(uint32_t) * 32;
+  static constexpr size_t bars_off = misc_off + sizeof(uint32_t) * 64;
+  static constexpr size_t info_off = bars_off + sizeof(uint64_t) * 2;
+  static constexpr size_t bytes = info_off + sizeof(InFlight) * 2;
 };
 
 template <typename K, int VB, int KIND, int BLOCK, int KPT>
 __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
   using S = LocalSmem<K, VB, KIND, BLOCK, KPT>;
+  using D = typename S::D;
   using V = typename S::V;
   constexpr int W = KeyTraits<K>::BITS;
-  extern __shared__ __align__(16) unsigned char smem[];
-  K *keys_s = reinterpret_cast<K *>(smem + S::keys_off);
-  V *vals_s = reinterpret_cast<V *>(smem + S::vals_off);
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned char *dbuf = smem + S::dbuf_off;
   uint32_t *whist_all = reinterpret_cast<uint32_t *>(smem + S::whist_off);
   uint32_t *tstart = reinterpret_cast<uint32_t *>(smem + S::tstart_off);
   uint64_t *red = reinterpret_cast<uint64_t *>(smem + S::red_off);
   uint32_t *misc = reinterpret_cast<uint32_t *>(smem + S::misc_off);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + S::bars_off);
+  InFlight *info = reinterpret_cast<InFlight *>(smem + S::info_off);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t ntasks = min(ws.ctl->ntasks, ws.maxtasks);
+  if (blockIdx.x >= ntasks) return;
   const KeyGeom<K, KIND> g{ws.shift0};
   uint32_t *whist = whist_all + w * 256;
+
+  auto prepare = [&](int slot, uint32_t ti) {
+    InFlight f{};
+    f.idx = ti;
+    f.valid = 0;
+    if (ti < ntasks) {
+      const Task tk = ws.tasks[ti];
+      f.start = tk.start;
+      f.cnt = tk.count;
+      f.parity = tk.parity;
+      f.valid = 1;
+      issue_copy<K, VB, S::CAP>(ws, dbuf, bars, slot, f);
+    }
+    info[slot] = f;
+  };
+
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+    prepare(0, blockIdx.x);
+  }
+  uint32_t phase = 0;
+  int cur = 0;
   for (uint32_t ti = blockIdx.x; ti < ntasks; ti += gridDim.x) {
-    const Task tk = ws.tasks[ti];
-    const int n = int(tk.count);
+    __syncthreads();  // previous task fully consumed; info[cur] visible
+    if (tid == 0) prepare(cur ^ 1, ti + gridDim.x);
+    const InFlight f = info[cur];
+    mbar_wait(&bars[cur], (phase >> cur) & 1u);
+    phase ^= 1u << cur;
+    K *kb = D::keys(dbuf, cur);
+    V *vbp = D::vals(dbuf, cur);
+    const int n = int(f.cnt);
     const int kk = (n + BLOCK - 1) / BLOCK;  // elements per thread for this task
     const int wbase = w * 32 * kk;
     const int nvw = max(0, min(32 * kk, n - wbase));
-    const K *src = static_cast<const K *>(ws.keys[tk.parity]) + tk.start;
-    K *dst = static_cast<K *>(ws.keys[0]) + tk.start;
-    const V *vsrc = VB ? static_cast<const V *>(ws.vals[tk.parity]) + tk.start : nullptr;
-    V *vdst = VB ? static_cast<V *>(ws.vals[0]) + tk.start : nullptr;
+    K *dst = static_cast<K *>(ws.keys[0]) + f.start;
+    V *vdst = VB ? static_cast<V *>(ws.vals[0]) + f.start : nullptr;
     K x[KPT];
     V v[KPT];
     K o = 0, a = ~K(0);
@@ -645,8 +830,8 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
       const int e = wbase + 32 * j + lane;
       x[j] = 0;
       if (32 * j + lane < nvw) {
-        x[j] = __ldcs(src + e);
-        if constexpr (VB != 0) v[j] = __ldcs(vsrc + e);
+        x[j] = kb[f.headk + e];
+        if constexpr (VB != 0) v[j] = vbp[f.headv + e];
         const K nk = g.norm(x[j]);
         o |= nk;
         a &= nk;
@@ -659,7 +844,7 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
       red[S::NW + w] = a;
     }
     __syncthreads();
-    K var;
+    K var, common;
     {
       K oo = 0, aa = ~K(0);
 #pragma unroll
@@ -668,9 +853,10 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
         aa &= K(red[S::NW + i]);
       }
       var = oo ^ aa;
+      common = oo;
     }
     if (var == 0) {
-      if (tk.parity) {
+      if (f.parity) {
 #pragma unroll
         for (int j = 0; j < KPT; ++j) {
           if (j >= kk) break;
@@ -681,71 +867,142 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
           }
         }
       }
-      __syncthreads();
+      cur ^= 1;
       continue;
     }
-    // digits that vary, least significant first
-    const int lastd = (W - 1 - (__ffsll((long long)(uint64_t(var))) - 1)) >> 3;
-    const int firstd = KeyTraits<K>::clz(var) >> 3;
-    bool first = true;
-    for (int dig = lastd; dig >= firstd; --dig) {
-      if (((var >> (W - 8 - 8 * dig)) & K(0xFF)) == 0) continue;
-      if (!first) {
-        // reload in element order from the previous pass
+    bool done = false;
+    if constexpr (VB == 0) {
+      const int lb = __ffsll((long long)(uint64_t(var))) - 1;
+      const int span = W - KeyTraits<K>::clz(var) - lb;
+      if (ws.shift0 == 0 && span <= 16) {
+        uint32_t *B1 = whist_all;
+        uint32_t *B2 = B1 + S::BM_WORDS;
+        uint32_t *EX = B2 + S::BM_WORDS;
+        uint32_t *OVF = EX + S::BM_WORDS;
+        uint32_t *novf = OVF + S::OVF_CAP;
+        const int nwords = span <= 5 ? 1 : (1 << (span - 5));
+        for (int i = tid; i < nwords; i += BLOCK) {
+          B1[i] = 0;
+          B2[i] = 0;
+          EX[i] = 0;
+        }
+        if (tid == 0) *novf = 0;
+        __syncthreads();
+        const K spanmask = (span >= W ? ~K(0) : ((K(1) << span) - 1)) << lb;
+        const K cbits = common & ~spanmask;
 #pragma unroll
         for (int j = 0; j < KPT; ++j) {
           if (j >= kk) break;
-          const int e = wbase + 32 * j + lane;
           if (32 * j + lane < nvw) {
-            x[j] = keys_s[e];
-            if constexpr (VB != 0) v[j] = vals_s[e];
+            const uint32_t idx = uint32_t((g.norm(x[j]) & spanmask) >> lb);
+            const uint32_t bit = 1u << (idx & 31);
+            if (atomicOr(&B1[idx >> 5], bit) & bit) {
+              if (atomicOr(&B2[idx >> 5], bit) & bit) {
+                atomicAdd(&EX[idx >> 5], 1u);
+                const uint32_t sl = atomicAdd(novf, 1u);
+                if (sl < S::OVF_CAP) OVF[sl] = idx;
+              }
+            }
           }
         }
         __syncthreads();
+        const uint32_t nov = *novf;
+        if (nov <= S::OVF_CAP) {
+          const int wpt = (nwords + BLOCK - 1) / BLOCK;
+          const int w0 = min(nwords, tid * wpt), w1 = min(nwords, w0 + wpt);
+          uint32_t c = 0;
+          for (int q = w0; q < w1; ++q) c += __popc(B1[q]) + __popc(B2[q]) + EX[q];
+          uint32_t pos = block_scan_excl<BLOCK>(c, misc);
+          for (int q = w0; q < w1; ++q) {
+            uint32_t b1 = B1[q];
+            const uint32_t b2 = B2[q];
+            const uint32_t ex = EX[q];
+            while (b1) {
+              const int bit = __ffs(b1) - 1;
+              b1 &= b1 - 1;
+              const uint32_t idx = uint32_t(q) * 32u + uint32_t(bit);
+              const K key = denorm<K, KIND>(cbits | (K(idx) << lb));
+              kb[pos++] = key;
+              if ((b2 >> bit) & 1u) {
+                kb[pos++] = key;
+                if (ex) {
+                  for (uint32_t i = 0; i < nov; ++i)
+                    if (OVF[i] == idx) kb[pos++] = key;
+                }
+              }
+            }
+          }
+          __syncthreads();
+          done = true;
+        }
+        // else: too many repeats for the overflow list -> LSD passes below
       }
-      const bool atomic_pass = (VB == 0) && first;
-      Ranks<KPT> rk;
-      rk.clear();
-      if (atomic_pass) {
-        if (tid < 256) whist_all[tid] = 0;
+    }
+    if (!done) {
+      // digits that vary, least significant first
+      const int lastd = (W - 1 - (__ffsll((long long)(uint64_t(var))) - 1)) >> 3;
+      const int firstd = KeyTraits<K>::clz(var) >> 3;
+      bool first = true;
+      for (int dig = lastd; dig >= firstd; --dig) {
+        if (((var >> (W - 8 - 8 * dig)) & K(0xFF)) == 0) continue;
+        if (!first) {
+          // reload in element order from the previous pass
+#pragma unroll
+          for (int j = 0; j < KPT; ++j) {
+            if (j >= kk) break;
+            const int e = wbase + 32 * j + lane;
+            if (32 * j + lane < nvw) {
+              x[j] = kb[e];
+              if constexpr (VB != 0) v[j] = vbp[e];
+            }
+          }
+          __syncthreads();
+        }
+        const bool atomic_pass = (VB == 0) && first;
+        Ranks<KPT> rk;
+        rk.clear();
+        if (atomic_pass) {
+          if (tid < 256) whist_all[tid] = 0;
+          __syncthreads();
+#pragma unroll
+          for (int j = 0; j < KPT; ++j) {
+            if (j >= kk) break;
+            if (32 * j + lane < nvw) rk.set(j, atomicAdd(&whist_all[g.digit(x[j], dig)], 1u));
+          }
+        } else {
+#pragma unroll
+          for (int i = lane; i < 256; i += 32) whist[i] = 0;
+          __syncwarp();
+          uint32_t dg[KPT];
+#pragma unroll
+          for (int j = 0; j < KPT; ++j) dg[j] = (j < kk) ? g.digit(x[j], dig) : 0u;
+          warp_rank_stable<KPT>(dg, kk, nvw, whist, rk);
+        }
+        __syncthreads();
+        const uint32_t total =
+            atomic_pass ? ((tid < 256) ? whist_all[tid] : 0u) : warp_prefix<S::NW>(whist_all);
+        const uint32_t texcl = scan256_excl<BLOCK>(total, misc);
+        if (tid < 256) tstart[tid] = texcl;
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < KPT; ++j) {
           if (j >= kk) break;
-          if (32 * j + lane < nvw) rk.set(j, atomicAdd(&whist_all[g.digit(x[j], dig)], 1u));
+          if (32 * j + lane < nvw) {
+            const uint32_t d = g.digit(x[j], dig);
+            const uint32_t pos = tstart[d] + rk.get(j) + (atomic_pass ? 0u : whist[d]);
+            kb[pos] = x[j];
+            if constexpr (VB != 0) vbp[pos] = v[j];
+          }
         }
-      } else {
-#pragma unroll
-        for (int i = lane; i < 256; i += 32) whist[i] = 0;
-        __syncwarp();
-        uint32_t dg[KPT];
-#pragma unroll
-        for (int j = 0; j < KPT; ++j) dg[j] = (j < kk) ? g.digit(x[j], dig) : 0u;
-        warp_rank_stable<KPT>(dg, kk, nvw, whist, rk);
+        __syncthreads();
+        first = false;
       }
-      __syncthreads();
-      const uint32_t total = atomic_pass ? ((tid < 256) ? whist_all[tid] : 0u) : warp_prefix<S::NW>(whist_all);
-      const uint32_t texcl = scan256_excl<BLOCK>(total, misc);
-      if (tid < 256) tstart[tid] = texcl;
-      __syncthreads();
-#pragma unroll
-      for (int j = 0; j < KPT; ++j) {
-        if (j >= kk) break;
-        if (32 * j + lane < nvw) {
-          const uint32_t d = g.digit(x[j], dig);
-          const uint32_t pos = tstart[d] + rk.get(j) + (atomic_pass ? 0u : whist[d]);
-          keys_s[pos] = x[j];
-          if constexpr (VB != 0) vals_s[pos] = v[j];
-        }
-      }
-      __syncthreads();
-      first = false;
     }
     for (int e = tid; e < n; e += BLOCK) {
-      __stcs(dst + e, keys_s[e]);
-      if constexpr (VB != 0) __stcs(vdst + e, vals_s[e]);
+      __stcs(dst + e, kb[e]);
+      if constexpr (VB != 0) __stcs(vdst + e, vbp[e]);
     }
-    __syncthreads();
+    cur ^= 1;
   }
 }
 
