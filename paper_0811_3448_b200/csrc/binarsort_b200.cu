@@ -58,6 +58,7 @@ static int num_sms() {
 struct Tune {
   int sc_block, sc_kpt, lc_block, lc_kpt;
 };
+constexpr int SC_NBUF = 2;
 constexpr Tune tune_for(int kb, int vb) {
   return (kb + vb) <= 4 ? Tune{512, 16, 512, 16} : (kb + vb) < 16 ? Tune{256, 16, 512, 16} : Tune{256, 16, 512, 8};
 }
@@ -160,13 +161,17 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   ws.group_min = geo.group_min;
   ws.ndig = geo.ndig;
   ws.shift0 = int(sizeof(K) * 8) - width_eff;
+  ws.stable = VB != 0;
 
   constexpr Tune TN = tune_for(int(sizeof(K)), VB);
   constexpr int SC_BLOCK = TN.sc_block, SKPT = TN.sc_kpt, LC_BLOCK = TN.lc_block, LC_KPT = TN.lc_kpt;
   constexpr int HI_BLOCK = SC_BLOCK, HKPT = SKPT;  // histogram tiles == scatter tiles
   using SS = ScatterSmem<K, VB, KIND, SC_BLOCK, SKPT>;
+  using SW = ScatterWsSmem<K, KIND, SC_BLOCK, SKPT, SC_NBUF>;
   using LS = LocalSmem<K, VB, KIND, LC_BLOCK, LC_KPT>;
+  constexpr bool WSPEC = VB == 0;  // keys-only: warp-specialised scatter
   auto sc = scatter_kernel<K, VB, KIND, SC_BLOCK, SKPT>;
+  auto sw = scatter_ws_kernel<K, KIND, SC_BLOCK, SKPT, SC_NBUF>;
   auto lc = local_kernel<K, VB, KIND, LC_BLOCK, LC_KPT>;
   auto hk = hist_kernel<K, KIND, HI_BLOCK, HKPT>;
   static int sc_grid = 0, lc_grid = 0, hk_grid = 0;
@@ -175,8 +180,10 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   std::call_once(once, [&] {
     cudaError_t e1 = cudaFuncSetAttribute(sc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SS::bytes));
     cudaError_t e2 = cudaFuncSetAttribute(lc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(LS::bytes));
-    attr_err = e1 != cudaSuccess ? e1 : e2;
-    sc_grid = num_sms() * max_active(sc, SC_BLOCK, SS::bytes);
+    cudaError_t e3 = cudaFuncSetAttribute(sw, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SW::bytes));
+    attr_err = e1 != cudaSuccess ? e1 : (e2 != cudaSuccess ? e2 : e3);
+    sc_grid = WSPEC ? num_sms() * max_active(sw, SC_BLOCK + 32, SW::bytes)
+                    : num_sms() * max_active(sc, SC_BLOCK, SS::bytes);
     lc_grid = num_sms() * max_active(lc, LC_BLOCK, LS::bytes);
     hk_grid = num_sms() * max_active(hk, HI_BLOCK, 0);
   });
@@ -198,7 +205,8 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
       plan_kernel<K><<<num_sms() * 4, 256, 0, st>>>(ws, L);
       expand_kernel<<<num_sms() * 4, 256, 0, st>>>(ws, L + 1);
       mark(st);
-      sc<<<sc_grid, SC_BLOCK, SS::bytes, st>>>(ws, L);
+      if constexpr (WSPEC) sw<<<sc_grid, SC_BLOCK + 32, SW::bytes, st>>>(ws, L);
+      else sc<<<sc_grid, SC_BLOCK, SS::bytes, st>>>(ws, L);
       mark(st);
     }
   }

@@ -69,6 +69,20 @@ struct KeyGeom {
   }
 };
 
+// Digit `dig` of a raw word, precomputed shifts: ((enc(x) << l) >> r) & 0xFF,
+// with the signed codec's sign flip folded into digit 0.
+template <typename K, int KIND>
+struct DigitFn {
+  int l, r;
+  uint32_t flip;
+  __device__ __forceinline__ DigitFn(int shift0, int dig)
+      : l(shift0), r(KeyTraits<K>::BITS - 8 - 8 * dig), flip((KIND == 1 && dig == 0) ? 0x80u : 0u) {}
+  __device__ __forceinline__ uint32_t operator()(K x) const {
+    const K e = (KIND == 2) ? encode<K, 2>(x) : x;
+    return (uint32_t((e << l) >> r) & 0xFFu) ^ flip;
+  }
+};
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -206,6 +220,16 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// barrier among the first NT threads of the CTA (id 1; id 0 is __syncthreads)
+template <int NT>
+__device__ __forceinline__ void named_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
 }
 
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {

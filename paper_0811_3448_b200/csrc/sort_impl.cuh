@@ -23,6 +23,24 @@
 namespace bs {
 
 constexpr int MAXLEV = 9;  // >= max digits (8 for u64) + 1
+
+// Optional in-kernel phase timing (compile with -DBS_PROFILE; scratch builds
+// only): thread 0 of every CTA accumulates clock64 deltas per phase.
+#ifdef BS_PROFILE
+__device__ unsigned long long g_prof[16];
+#define BS_PROBE_INIT() long long prof_t0_ = clock64()
+#define BS_PROBE(i)                                                 \
+  do {                                                              \
+    if (threadIdx.x == 0) {                                         \
+      const long long now_ = clock64();                             \
+      atomicAdd(&g_prof[i], (unsigned long long)(now_ - prof_t0_)); \
+      prof_t0_ = now_;                                              \
+    }                                                               \
+  } while (0)
+#else
+#define BS_PROBE_INIT() (void)0
+#define BS_PROBE(i) (void)0
+#endif
 constexpr uint32_t ST_AGG = 1u << 30;
 constexpr uint32_t ST_INCL = 2u << 30;
 constexpr uint32_t ST_MASK = (1u << 30) - 1;
@@ -74,6 +92,7 @@ struct Ws {
   uint32_t group_min;  // children smaller than this are grouped
   int ndig;            // number of 8-bit digits of the effective key
   int shift0;          // W - width_eff
+  int stable;          // key-value sort: tiles use the look-back scan
 };
 
 
@@ -197,7 +216,7 @@ __global__ void __launch_bounds__(BLOCK) hist_kernel(Ws ws, int L) {
       dig = int(bk.digit);
     }
     // clear this tile's look-back row (256 x u32 = 64 x uint4)
-    if (tid < 64)
+    if (ws.stable && tid < 64)
       reinterpret_cast<uint4 *>(ws.status + size_t(t) * 256)[tid] = make_uint4(0, 0, 0, 0);
     const uint64_t off = uint64_t(t - bk.tile0) * ws.tile;
     const uint32_t cnt = uint32_t(min64(ws.tile, bk.count - off));
@@ -634,9 +653,12 @@ __global__ void __launch_bounds__(BLOCK) scatter_kernel(Ws ws, int L) {
     claim(0);
   }
   uint32_t phase = 0;  // bit i: parity of buffer i's next completion
+  BS_PROBE_INIT();
   int cur = 0;
   for (;;) {
-    if (tid == 0) claim(cur ^ 1);  // spare buffer is free: previous tile fully consumed
+    // keys-only tiles have no look-back, so the next tile is claimed (and
+    // its bulk copy started) as early as possible
+    if (!STABLE && tid == 0) claim(cur ^ 1);
     if constexpr (STABLE) {
 #pragma unroll
       for (int i = lane; i < 256; i += 32) whist[i] = 0;
@@ -647,85 +669,329 @@ __global__ void __launch_bounds__(BLOCK) scatter_kernel(Ws ws, int L) {
     const InFlight f = info[cur];
     if (f.idx >= nt) break;
     if (!f.valid) {
+      if (STABLE && tid == 0) claim(cur ^ 1);
       __syncthreads();
       cur ^= 1;
       continue;
     }
+    BS_PROBE(0);
     mbar_wait(&bars[cur], (phase >> cur) & 1u);
     phase ^= 1u << cur;
+    BS_PROBE(1);
     K *kb = D::keys(dbuf, cur);
     V *vbp = D::vals(dbuf, cur);
     const int cnt = int(f.cnt);
     const int dig = int(f.digit);
     const int wbase = w * 32 * KPT;
+    const DigitFn<K, KIND> dfn(ws.shift0, dig);
+    const bool full = cnt == TILE;  // all but the last tile of a bucket
     K x[KPT];
     V v[KPT];
     Ranks<KPT> rk;
     rk.clear();
+    if (full) {
 #pragma unroll
-    for (int j = 0; j < KPT; ++j) {
-      const int e = wbase + 32 * j + lane;
-      x[j] = 0;
-      if (e < cnt) {
+      for (int j = 0; j < KPT; ++j) {
+        const int e = wbase + 32 * j + lane;
         x[j] = kb[f.headk + e];
         if constexpr (VB != 0) v[j] = vbp[f.headv + e];
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < KPT; ++j) {
+        const int e = wbase + 32 * j + lane;
+        x[j] = 0;
+        if (e < cnt) {
+          x[j] = kb[f.headk + e];
+          if constexpr (VB != 0) v[j] = vbp[f.headv + e];
+        }
       }
     }
     if constexpr (STABLE) {
       uint32_t dg[KPT];
 #pragma unroll
-      for (int j = 0; j < KPT; ++j) dg[j] = g.digit(x[j], dig);
+      for (int j = 0; j < KPT; ++j) dg[j] = dfn(x[j]);
       warp_rank_stable<KPT>(dg, KPT, max(0, min(32 * KPT, cnt - wbase)), whist, rk);
+    } else if (full) {
+#pragma unroll
+      for (int j = 0; j < KPT; ++j) rk.set(j, atomicAdd(&whist[dfn(x[j])], 1u));
     } else {
 #pragma unroll
       for (int j = 0; j < KPT; ++j) {
         const int e = wbase + 32 * j + lane;
-        if (e < cnt) rk.set(j, atomicAdd(&whist[g.digit(x[j], dig)], 1u));
+        if (e < cnt) rk.set(j, atomicAdd(&whist[dfn(x[j])], 1u));
       }
     }
     __syncthreads();
+    BS_PROBE(2);
     uint32_t total;
     if constexpr (STABLE) total = warp_prefix<S::NW>(whist_all);
     else total = (tid < 256) ? whist[tid] : 0u;
-    // publish this tile's digit counts first so successors can look past it
-    uint32_t *st = ws.status + size_t(f.idx) * 256 + tid;
-    if (tid < 256) st_relaxed(st, (f.tin == 0 ? ST_INCL : ST_AGG) | total);
-    const uint32_t texcl = scan256_excl<BLOCK>(total, misc);
-    if (tid < 256) {
-      tstart[tid] = texcl;
-      uint32_t prefix = 0;
-      if (f.tin != 0) {
-        prefix = lookback(ws.status, f.idx, f.tile0, tid);
-        st_relaxed(st, ST_INCL | (prefix + total));
+    uint32_t texcl;
+    const uint32_t bucket_start = uint32_t(f.start - uint64_t(f.tin) * TILE);
+    if constexpr (STABLE) {
+      // Stable (key-value) sorts: tiles of a bucket must land in tile order,
+      // so the offsets come from a single-pass chained scan with decoupled
+      // look-back.  Publish this tile's counts first so successors can look
+      // past it.
+      uint32_t *st = ws.status + size_t(f.idx) * 256 + tid;
+      if (tid < 256) st_relaxed(st, (f.tin == 0 ? ST_INCL : ST_AGG) | total);
+      texcl = scan256_excl<BLOCK>(total, misc);
+      BS_PROBE(3);
+      if (tid < 256) {
+        tstart[tid] = texcl;
+        uint32_t prefix = 0;
+        if (f.tin != 0) {
+          prefix = lookback(ws.status, f.idx, f.tile0, tid);
+          st_relaxed(st, ST_INCL | (prefix + total));
+        }
+        // element offset of this tile's digit-d run minus its tile position
+        // (mod 2^32: true offsets are < n <= 2^30)
+        reinterpret_cast<uint32_t *>(gbase)[tid] =
+            bucket_start + ws.bhist[lv][size_t(f.b) * 256 + tid] + prefix - texcl;
       }
-      const uint64_t tile_bucket_start = f.start - uint64_t(f.tin) * TILE;
-      gbase[tid] = tile_bucket_start + uint64_t(ws.bhist[lv][size_t(f.b) * 256 + tid]) + prefix - texcl;
+    } else {
+      // Keys-only MSD: the order of keys inside a child bucket is irrelevant
+      // (the child is sorted completely later), so each tile reserves its run
+      // per digit with one atomic on the bucket's digit cursor (plan_kernel
+      // left the digit bases there) -- no chain across tiles at all.
+      uint32_t base = 0;
+      if (tid < 256 && total) base = atomicAdd(&ws.bhist[lv][size_t(f.b) * 256 + tid], total);
+      texcl = scan256_excl<BLOCK>(total, misc);
+      BS_PROBE(3);
+      if (tid < 256) {
+        tstart[tid] = texcl;
+        reinterpret_cast<uint32_t *>(gbase)[tid] = bucket_start + base - texcl;
+      }
     }
     __syncthreads();
+    BS_PROBE(4);
     // stage in digit order (the input buffer is consumed: keys are in registers)
+    auto stage = [&](int j) {
+      const uint32_t d = dfn(x[j]);
+      uint32_t pos = tstart[d] + rk.get(j);
+      if constexpr (STABLE) pos += whist[d];
+      kb[pos] = x[j];
+      if constexpr (VB != 0) vbp[pos] = v[j];
+    };
+    if (full) {
 #pragma unroll
-    for (int j = 0; j < KPT; ++j) {
-      const int e = wbase + 32 * j + lane;
-      if (e < cnt) {
-        const uint32_t d = g.digit(x[j], dig);
-        uint32_t pos = tstart[d] + rk.get(j);
-        if constexpr (STABLE) pos += whist[d];
-        kb[pos] = x[j];
-        if constexpr (VB != 0) vbp[pos] = v[j];
-      }
+      for (int j = 0; j < KPT; ++j) stage(j);
+    } else {
+#pragma unroll
+      for (int j = 0; j < KPT; ++j)
+        if (wbase + 32 * j + lane < cnt) stage(j);
     }
     __syncthreads();
+    BS_PROBE(5);
+    // Stable sorts claim the next tile only now: a claimed-but-unranked tile
+    // would stall its successors' look-back.  Its copy overlaps this write-out.
+    if (STABLE && tid == 0) claim(cur ^ 1);
     K *dst = static_cast<K *>(ws.keys[f.parity ^ 1]);
     V *vdst = VB ? static_cast<V *>(ws.vals[f.parity ^ 1]) : nullptr;
-#pragma unroll 4
-    for (int e = tid; e < cnt; e += BLOCK) {
-      const K k = kb[e];
-      const uint64_t o = gbase[g.digit(k, dig)] + uint64_t(e);
-      __stcs(dst + o, k);
-      if constexpr (VB != 0) __stcs(vdst + o, vbp[e]);
+    const uint32_t *gb = reinterpret_cast<const uint32_t *>(gbase);
+    if (full) {
+#pragma unroll
+      for (int j = 0; j < KPT; ++j) {
+        const int e = j * BLOCK + tid;
+        const K k = kb[e];
+        const uint32_t o = gb[dfn(k)] + uint32_t(e);
+        __stcs(dst + o, k);
+        if constexpr (VB != 0) __stcs(vdst + o, vbp[e]);
+      }
+    } else {
+      for (int e = tid; e < cnt; e += BLOCK) {
+        const K k = kb[e];
+        const uint32_t o = gb[dfn(k)] + uint32_t(e);
+        __stcs(dst + o, k);
+        if constexpr (VB != 0) __stcs(vdst + o, vbp[e]);
+      }
     }
+#ifdef BS_PROFILE
     __syncthreads();
+#endif
+    BS_PROBE(6);
     cur ^= 1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Keys-only scatter, warp-specialised.  One producer warp claims tiles and
+// streams them in with TMA bulk copies through a ring of NBUF shared buffers
+// (full/empty mbarriers); BLOCK consumer threads rank (shared atomics),
+// reserve each digit run with one global atomic per digit, stage the tile in
+// digit order in the consumed buffer and write it out coalesced.  Claim
+// latency and copy latency both hide behind the consumers' work.
+// ---------------------------------------------------------------------------
+template <typename K, int KIND, int BLOCK, int KPT, int NBUF>
+struct ScatterWsSmem {
+  static constexpr int TILE = BLOCK * KPT;
+  static constexpr size_t kbuf = (sizeof(K) * TILE + 32 + 15) & ~size_t(15);
+  static constexpr size_t dbuf_off = 0;
+  static constexpr size_t cnt_off = dbuf_off + NBUF * kbuf;
+  static constexpr size_t gbase_off = cnt_off + sizeof(uint32_t) * 256;
+  static constexpr size_t tstart_off = gbase_off + sizeof(uint32_t) * 256;
+  static constexpr size_t misc_off = tstart_off + sizeof(uint32_t) * 256;
+  static constexpr size_t bars_off = misc_off + sizeof(uint32_t) * 64;
+  static constexpr size_t info_off = bars_off + sizeof(uint64_t) * 2 * NBUF;
+  static constexpr size_t bytes = info_off + sizeof(InFlight) * NBUF;
+};
+
+// 256-bin exclusive scan among the BLOCK consumer threads (named barrier 1)
+template <int BLOCK>
+__device__ __forceinline__ uint32_t scan256_excl_nb(uint32_t v, uint32_t *scratch) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t x = (tid < 256) ? v : 0u;
+  uint32_t incl = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (tid < 256 && lane == 31) scratch[w] = incl;
+  named_sync<BLOCK>();
+  if (tid < 32) {
+    const uint32_t s = (lane < 8) ? scratch[lane] : 0u;
+    uint32_t si = s;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, si, o);
+      if (lane >= o) si += y;
+    }
+    if (lane < 8) scratch[lane] = si - s;
+  }
+  named_sync<BLOCK>();
+  return (tid < 256) ? scratch[w] + incl - x : 0u;
+}
+
+template <typename K, int KIND, int BLOCK, int KPT, int NBUF>
+__global__ void __launch_bounds__(BLOCK + 32) scatter_ws_kernel(Ws ws, int L) {
+  using S = ScatterWsSmem<K, KIND, BLOCK, KPT, NBUF>;
+  constexpr int TILE = S::TILE;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint32_t *cnt256 = reinterpret_cast<uint32_t *>(smem + S::cnt_off);
+  uint32_t *gbase = reinterpret_cast<uint32_t *>(smem + S::gbase_off);
+  uint32_t *tstart = reinterpret_cast<uint32_t *>(smem + S::tstart_off);
+  uint32_t *misc = reinterpret_cast<uint32_t *>(smem + S::misc_off);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + S::bars_off);
+  uint64_t *empty = full + NBUF;
+  InFlight *info = reinterpret_cast<InFlight *>(smem + S::info_off);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int lv = L & 1;
+  const uint32_t nt = ws.ctl->ntiles[L];
+  if (nt == 0) return;
+  if (tid == BLOCK) {
+    for (int i = 0; i < NBUF; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (w == BLOCK / 32) {  // ---------------- producer warp ----------------
+    if (lane != 0) return;
+    for (uint32_t i = 0;; ++i) {
+      const int s = int(i % NBUF);
+      if (i >= NBUF) mbar_wait(&empty[s], ((i / NBUF) - 1) & 1u);
+      InFlight f{};
+      f.idx = atomicAdd(&ws.ctl->ticket[L], 1u);
+      if (f.idx < nt) {
+        const uint32_t b = ws.tile_bucket[lv][f.idx];
+        const Bucket bk = ws.buckets[lv][b];
+        f.b = b;
+        f.tin = f.idx - bk.tile0;
+        f.digit = bk.digit;
+        f.parity = bk.parity;
+        const uint64_t off = uint64_t(f.tin) * TILE;
+        f.start = bk.start + off;
+        f.cnt = uint32_t(min64(TILE, bk.count - off));
+        f.valid = bk.action == ACT_SCATTER;
+      }
+      if (f.valid) {
+        const Span sk = span16(static_cast<const K *>(ws.keys[f.parity]) + f.start, f.cnt);
+        f.headk = sk.head;
+        info[s] = f;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&full[s], sk.bytes);
+        bulk_g2s(smem + S::dbuf_off + s * S::kbuf, sk.base, sk.bytes, &full[s]);
+      } else {
+        info[s] = f;
+        mbar_arrive(&full[s]);
+      }
+      if (f.idx >= nt) return;
+    }
+  }
+
+  // ---------------- consumers ----------------
+  for (uint32_t i = 0;; ++i) {
+    const int s = int(i % NBUF);
+    mbar_wait(&full[s], (i / NBUF) & 1u);
+    const InFlight f = info[s];
+    if (f.idx >= nt) break;
+    if (f.valid) {
+      K *kb = reinterpret_cast<K *>(smem + S::dbuf_off + s * S::kbuf);
+      const int cnt = int(f.cnt);
+      const DigitFn<K, KIND> dfn(ws.shift0, int(f.digit));
+      const bool fullt = cnt == TILE;
+      if (tid < 256) cnt256[tid] = 0;
+      named_sync<BLOCK>();
+      // count (shared RED), scan, then place by atomic cursors -- no ranks
+      // kept in registers, no per-key lookup of the tile digit start
+      K x[KPT];
+      if (fullt) {
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+          x[j] = kb[f.headk + j * BLOCK + tid];
+          atomicAdd(&cnt256[dfn(x[j])], 1u);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+          const int e = j * BLOCK + tid;
+          x[j] = 0;
+          if (e < cnt) {
+            x[j] = kb[f.headk + e];
+            atomicAdd(&cnt256[dfn(x[j])], 1u);
+          }
+        }
+      }
+      named_sync<BLOCK>();
+      const uint32_t total = (tid < 256) ? cnt256[tid] : 0u;
+      uint32_t base = 0;
+      if (tid < 256 && total) base = atomicAdd(&ws.bhist[lv][size_t(f.b) * 256 + tid], total);
+      const uint32_t texcl = scan256_excl_nb<BLOCK>(total, misc);
+      if (tid < 256) {
+        tstart[tid] = texcl;  // becomes the staging cursor of digit tid
+        gbase[tid] = uint32_t(f.start - uint64_t(f.tin) * TILE) + base - texcl;
+      }
+      named_sync<BLOCK>();
+      if (fullt) {
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) kb[atomicAdd(&tstart[dfn(x[j])], 1u)] = x[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < KPT; ++j)
+          if (j * BLOCK + tid < cnt) kb[atomicAdd(&tstart[dfn(x[j])], 1u)] = x[j];
+      }
+      named_sync<BLOCK>();
+      K *dst = static_cast<K *>(ws.keys[f.parity ^ 1]);
+      if (fullt) {
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+          const int e = j * BLOCK + tid;
+          const K k = kb[e];
+          __stcs(dst + (gbase[dfn(k)] + uint32_t(e)), k);
+        }
+      } else {
+        for (int e = tid; e < cnt; e += BLOCK) {
+          const K k = kb[e];
+          __stcs(dst + (gbase[dfn(k)] + uint32_t(e)), k);
+        }
+      }
+    }
+    named_sync<BLOCK>();  // every consumer is done with buffer s
+    if (tid == 0) mbar_arrive(&empty[s]);
   }
 }
 
@@ -755,7 +1021,7 @@ struct LocalSmem {
   static constexpr size_t dbuf_off = 0;
   static constexpr size_t whist_off = dbuf_off + D::bytes;
   static constexpr size_t whist_bytes = sizeof(uint32_t) * NW * 256;
-  static constexpr size_t bm_bytes = VB ? 0 : sizeof(uint32_t) * (3 * BM_WORDS + OVF_CAP + 4);
+  static constexpr size_t bm_bytes = VB ? 0 : sizeof(uint32_t) * (4 * BM_WORDS + OVF_CAP + 4);
   static constexpr size_t tstart_off = whist_off + (whist_bytes > bm_bytes ? whist_bytes : bm_bytes);
   static constexpr size_t red_off = tstart_off + sizeof(uint32_t) * 256;
   static constexpr size_t misc_off = red_off + sizeof(uint64_t) * 2 * NW;
@@ -875,10 +1141,13 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
       const int lb = __ffsll((long long)(uint64_t(var))) - 1;
       const int span = W - KeyTraits<K>::clz(var) - lb;
       if (ws.shift0 == 0 && span <= 16) {
+        // B1: value present, B2: a second copy, EX: per-word count of further
+        // copies (listed in OVF), WP: per-word exclusive prefix of all copies.
         uint32_t *B1 = whist_all;
         uint32_t *B2 = B1 + S::BM_WORDS;
         uint32_t *EX = B2 + S::BM_WORDS;
-        uint32_t *OVF = EX + S::BM_WORDS;
+        uint32_t *WP = EX + S::BM_WORDS;
+        uint32_t *OVF = WP + S::BM_WORDS;
         uint32_t *novf = OVF + S::OVF_CAP;
         const int nwords = span <= 5 ? 1 : (1 << (span - 5));
         for (int i = tid; i < nwords; i += BLOCK) {
@@ -889,7 +1158,8 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
         if (tid == 0) *novf = 0;
         __syncthreads();
         const K spanmask = (span >= W ? ~K(0) : ((K(1) << span) - 1)) << lb;
-        const K cbits = common & ~spanmask;
+        Ranks<KPT> cp;  // copy index: 0 first, 1 second, 2 + overflow slot
+        cp.clear();
 #pragma unroll
         for (int j = 0; j < KPT; ++j) {
           if (j >= kk) break;
@@ -897,11 +1167,14 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
             const uint32_t idx = uint32_t((g.norm(x[j]) & spanmask) >> lb);
             const uint32_t bit = 1u << (idx & 31);
             if (atomicOr(&B1[idx >> 5], bit) & bit) {
+              uint32_t c = 1;
               if (atomicOr(&B2[idx >> 5], bit) & bit) {
                 atomicAdd(&EX[idx >> 5], 1u);
                 const uint32_t sl = atomicAdd(novf, 1u);
                 if (sl < S::OVF_CAP) OVF[sl] = idx;
+                c = 2 + min(sl, uint32_t(S::OVF_CAP));
               }
+              cp.set(j, c);
             }
           }
         }
@@ -912,24 +1185,29 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
           const int w0 = min(nwords, tid * wpt), w1 = min(nwords, w0 + wpt);
           uint32_t c = 0;
           for (int q = w0; q < w1; ++q) c += __popc(B1[q]) + __popc(B2[q]) + EX[q];
-          uint32_t pos = block_scan_excl<BLOCK>(c, misc);
+          uint32_t run = block_scan_excl<BLOCK>(c, misc);
           for (int q = w0; q < w1; ++q) {
-            uint32_t b1 = B1[q];
-            const uint32_t b2 = B2[q];
-            const uint32_t ex = EX[q];
-            while (b1) {
-              const int bit = __ffs(b1) - 1;
-              b1 &= b1 - 1;
-              const uint32_t idx = uint32_t(q) * 32u + uint32_t(bit);
-              const K key = denorm<K, KIND>(cbits | (K(idx) << lb));
-              kb[pos++] = key;
-              if ((b2 >> bit) & 1u) {
-                kb[pos++] = key;
-                if (ex) {
-                  for (uint32_t i = 0; i < nov; ++i)
-                    if (OVF[i] == idx) kb[pos++] = key;
+            WP[q] = run;
+            run += __popc(B1[q]) + __popc(B2[q]) + EX[q];
+          }
+          __syncthreads();
+          // each key's position = copies of smaller values + its copy index
+#pragma unroll
+          for (int j = 0; j < KPT; ++j) {
+            if (j >= kk) break;
+            if (32 * j + lane < nvw) {
+              const uint32_t idx = uint32_t((g.norm(x[j]) & spanmask) >> lb);
+              const uint32_t q = idx >> 5, low = (1u << (idx & 31)) - 1u;
+              uint32_t pos = WP[q] + __popc(B1[q] & low) + __popc(B2[q] & low);
+              const uint32_t c = cp.get(j);
+              if (EX[q]) {  // rare: >= 3 copies of some value in this word
+                for (uint32_t i = 0; i < nov; ++i) {
+                  const uint32_t o = OVF[i];
+                  pos += ((o >> 5) == q && o < idx) ? 1u : 0u;
+                  pos += (c >= 2 && o == idx && i < c - 2) ? 1u : 0u;
                 }
               }
+              kb[pos + (c < 2 ? c : 2u)] = x[j];
             }
           }
           __syncthreads();
