@@ -93,7 +93,7 @@ static Geometry geometry(uint64_t n, int kb, int vb, int width_eff) {
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t ctl, buckets[2], bhist[2], bor[2], band[2], tile_bucket[2], status, tasks, keys, vals, total;
+  size_t ctl, buckets[2], bhist[2], bor[2], band[2], tile_bucket[2], status, tasks, dtasks, keys, vals, total;
 };
 
 static Layout layout(const Geometry &g) {
@@ -114,6 +114,7 @@ static Layout layout(const Geometry &g) {
   }
   l.status = take(sizeof(uint32_t) * 256 * size_t(g.maxtiles));
   l.tasks = take(sizeof(Task) * g.maxtasks);
+  l.dtasks = take(g.vb == 0 ? sizeof(DTask) * g.maxtasks : 0);
   l.keys = take(size_t(g.kb) * g.n);
   l.vals = take(size_t(g.vb) * g.n);
   l.total = off;
@@ -148,6 +149,7 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   }
   ws.status = reinterpret_cast<uint32_t *>(base + lay.status);
   ws.tasks = reinterpret_cast<Task *>(base + lay.tasks);
+  ws.dtasks = reinterpret_cast<DTask *>(base + lay.dtasks);
   ws.keys[0] = keys;
   ws.keys[1] = base + lay.keys;
   ws.vals[0] = vals;
@@ -162,6 +164,7 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   ws.ndig = geo.ndig;
   ws.shift0 = int(sizeof(K) * 8) - width_eff;
   ws.stable = VB != 0;
+  ws.dense = (VB == 0 && width_eff == int(sizeof(K) * 8)) ? 1 : 0;
 
   constexpr Tune TN = tune_for(int(sizeof(K)), VB);
   constexpr int SC_BLOCK = TN.sc_block, SKPT = TN.sc_kpt, LC_BLOCK = TN.lc_block, LC_KPT = TN.lc_kpt;
@@ -172,16 +175,24 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   constexpr bool WSPEC = VB == 0;  // keys-only: warp-specialised scatter
   auto sc = scatter_kernel<K, VB, KIND, SC_BLOCK, SKPT>;
   auto sw = scatter_ws_kernel<K, KIND, SC_BLOCK, SKPT, SC_NBUF>;
+  // dense local sort: 512 consumers x 12 keys (6144-key tasks), 2-slot ring
+  constexpr int DN_BLOCK = 512, DN_KPT = 12, DN_SLOTS = 2;
+  using DS = DenseSmem<K, DN_BLOCK, DN_KPT, DN_SLOTS>;
+  auto dk = dense_kernel<K, KIND, DN_BLOCK, DN_KPT, DN_SLOTS>;
+  ws.dense_max = DN_BLOCK * DN_KPT;
   auto lc = local_kernel<K, VB, KIND, LC_BLOCK, LC_KPT>;
   auto hk = hist_kernel<K, KIND, HI_BLOCK, HKPT>;
-  static int sc_grid = 0, lc_grid = 0, hk_grid = 0;
+  static int sc_grid = 0, lc_grid = 0, hk_grid = 0, dk_grid = 0;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
     cudaError_t e1 = cudaFuncSetAttribute(sc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SS::bytes));
     cudaError_t e2 = cudaFuncSetAttribute(lc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(LS::bytes));
     cudaError_t e3 = cudaFuncSetAttribute(sw, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SW::bytes));
-    attr_err = e1 != cudaSuccess ? e1 : (e2 != cudaSuccess ? e2 : e3);
+    cudaError_t e4 = VB == 0 ? cudaFuncSetAttribute(dk, cudaFuncAttributeMaxDynamicSharedMemorySize, int(DS::bytes))
+                             : cudaSuccess;
+    attr_err = e1 != cudaSuccess ? e1 : (e2 != cudaSuccess ? e2 : (e3 != cudaSuccess ? e3 : e4));
+    dk_grid = VB == 0 ? num_sms() * max_active(dk, DN_BLOCK + 32, DS::bytes) : 0;
     sc_grid = WSPEC ? num_sms() * max_active(sw, SC_BLOCK + 32, SW::bytes)
                     : num_sms() * max_active(sc, SC_BLOCK, SS::bytes);
     lc_grid = num_sms() * max_active(lc, LC_BLOCK, LS::bytes);
@@ -209,6 +220,9 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
       else sc<<<sc_grid, SC_BLOCK, SS::bytes, st>>>(ws, L);
       mark(st);
     }
+  }
+  if constexpr (VB == 0) {
+    if (ws.dense) dk<<<dk_grid, DN_BLOCK + 32, DS::bytes, st>>>(ws);
   }
   lc<<<lc_grid, LC_BLOCK, LS::bytes, st>>>(ws);
   mark(st);
@@ -321,7 +335,7 @@ int bs_sort_launches(uint64_t n, int key_bytes, int width, int start_pos, int wi
   const int width_eff = width - start_pos;
   if (n <= 1 || width_eff <= 0) return 0;
   const Geometry g = geometry(n, key_bytes, 0, width_eff);
-  int k = 2;  // init + local
+  int k = 3;  // init + dense + local
   if (n > g.local_max) k += 4 * (g.ndig + 1);
   if (with_counters) k += 2;
   return k;

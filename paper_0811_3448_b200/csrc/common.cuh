@@ -240,6 +240,19 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       : "memory");
 }
 
+// Producer-side wait: back off between polls so a spinning producer lane does
+// not steal issue slots from the consumer warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+  // try_wait with a suspend-time hint: the waiting thread is descheduled
+  // until the phase completes (or ~1 ms passes) instead of polling
+  asm volatile(
+      "{\n .reg .pred p;\n WAITS_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
+      " @!p bra WAITS_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"

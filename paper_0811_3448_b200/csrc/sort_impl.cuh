@@ -28,18 +28,26 @@ constexpr int MAXLEV = 9;  // >= max digits (8 for u64) + 1
 // only): thread 0 of every CTA accumulates clock64 deltas per phase.
 #ifdef BS_PROFILE
 __device__ unsigned long long g_prof[16];
-#define BS_PROBE_INIT() long long prof_t0_ = clock64()
-#define BS_PROBE(i)                                                 \
-  do {                                                              \
-    if (threadIdx.x == 0) {                                         \
-      const long long now_ = clock64();                             \
-      atomicAdd(&g_prof[i], (unsigned long long)(now_ - prof_t0_)); \
-      prof_t0_ = now_;                                              \
-    }                                                               \
+// deltas accumulate in registers; BS_PROBE_FLUSH() publishes them once
+#define BS_PROBE_INIT()          \
+  long long prof_t0_ = clock64(); \
+  long long prof_acc_[16] = {0}
+#define BS_PROBE(i)                        \
+  do {                                     \
+    const long long now_ = clock64();      \
+    prof_acc_[i] += now_ - prof_t0_;       \
+    prof_t0_ = now_;                       \
+  } while (0)
+#define BS_PROBE_FLUSH()                                                            \
+  do {                                                                              \
+    if (threadIdx.x == 0)                                                           \
+      for (int i_ = 0; i_ < 16; ++i_)                                               \
+        if (prof_acc_[i_]) atomicAdd(&g_prof[i_], (unsigned long long)prof_acc_[i_]); \
   } while (0)
 #else
 #define BS_PROBE_INIT() (void)0
 #define BS_PROBE(i) (void)0
+#define BS_PROBE_FLUSH() (void)0
 #endif
 constexpr uint32_t ST_AGG = 1u << 30;
 constexpr uint32_t ST_INCL = 2u << 30;
@@ -63,12 +71,21 @@ struct Task {
   uint32_t parity;
 };
 
+// A dense keys-only task: every key equals `common` outside the bit span
+// [lb, lb+span) of the normalised key (span <= 16).
+struct DTask {
+  uint64_t start;
+  uint64_t common;
+  uint32_t count;
+  uint32_t meta;  // lb | span << 8 | parity << 16
+};
+
 struct Ctl {
   uint32_t nbuckets[MAXLEV + 1];
   uint32_t ntiles[MAXLEV + 1];
   uint32_t ticket[MAXLEV + 1];
   uint32_t ntasks;
-  uint32_t task_ticket;
+  uint32_t ndtasks;
   uint32_t error;  // bit 0: bucket overflow, 1: tile overflow, 2: task overflow
   uint32_t pad;
 };
@@ -83,6 +100,9 @@ struct Ws {
   uint32_t *tile_bucket[2];
   uint32_t *status;  // [maxtiles][256]
   Task *tasks;
+  DTask *dtasks;
+  int dense;           // keys-only full-width: dense tasks go to dense_kernel
+  uint32_t dense_max;  // dense_kernel capacity
   void *keys[2];  // [0] caller's buffer, [1] workspace copy
   void *vals[2];
   uint64_t n;
@@ -251,7 +271,8 @@ __global__ void __launch_bounds__(BLOCK) hist_kernel(Ws ws, int L) {
 struct Emit {
   uint64_t start;
   uint32_t count;
-  uint32_t kind;  // 0 large child (next level), 1 local task
+  uint32_t kind;   // 0 large child (next level), 1 local task
+  uint32_t digit;  // the child's digit value, or 0xFFFFFFFF for a group of children
 };
 
 __device__ __forceinline__ void emit_tasks(const Ws &ws, uint64_t start, uint64_t count,
@@ -339,12 +360,12 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
         const uint32_t cd = s_cnt[d];
         if (cd == 0) continue;
         if (cd >= ws.group_min) {
-          if (gc) s_emit[ne++] = Emit{gs, gc, 1};
+          if (gc) s_emit[ne++] = Emit{gs, gc, 1, 0xFFFFFFFFu};
           gc = 0;
-          s_emit[ne++] = Emit{pos, cd, cd > ws.local_max ? 0u : 1u};
+          s_emit[ne++] = Emit{pos, cd, cd > ws.local_max ? 0u : 1u, uint32_t(d)};
         } else {
           if (gc + cd > ws.local_max) {
-            s_emit[ne++] = Emit{gs, gc, 1};
+            s_emit[ne++] = Emit{gs, gc, 1, 0xFFFFFFFFu};
             gc = 0;
           }
           if (gc == 0) gs = pos;
@@ -352,15 +373,32 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
         }
         pos += cd;
       }
-      if (gc) s_emit[ne++] = Emit{gs, gc, 1};
+      if (gc) s_emit[ne++] = Emit{gs, gc, 1, 0xFFFFFFFFu};
       s_nemit = ne;
     }
     __syncthreads();
     const uint32_t ne = s_nemit;
+    // standalone children whose varying bits fit a 16-bit span are dense tasks
+    const int lbv = __ffsll((long long)uint64_t(lower)) - 1;
+    const int spanv = W - KeyTraits<K>::clz(lower) - lbv;
+    const bool dense = ws.dense && spanv <= 16;
+    const K spanmask = (spanv >= W ? ~K(0) : ((K(1) << spanv) - 1)) << lbv;
+    const K dmask = K(0xFF) << lowbits;
+    const K cbase = K(ws.bor[cur][b]) & ~spanmask & ~dmask;
     for (uint32_t i = tid; i < ne; i += 256) {
       const Emit e = s_emit[i];
       if (e.kind == 1) {
-        if (!(e.count == 1 && cpar == 0)) emit_tasks(ws, e.start, e.count, cpar);  // singleton home: done
+        if (e.count == 1 && cpar == 0) continue;  // singleton already home: done
+        if (dense && e.digit != 0xFFFFFFFFu && e.count > 1 && e.count <= ws.dense_max) {
+          const uint32_t slot = atomicAdd(&ws.ctl->ndtasks, 1u);
+          if (slot < ws.maxtasks)
+            ws.dtasks[slot] = DTask{e.start, uint64_t(cbase | (K(e.digit) << lowbits)), e.count,
+                                    uint32_t(lbv) | (uint32_t(spanv) << 8) | (cpar << 16)};
+          else
+            atomicOr(&ws.ctl->error, 4u);
+        } else {
+          emit_tasks(ws, e.start, e.count, cpar);
+        }
       } else {
         push_bucket(ws, L, e.start, e.count, uint32_t(dig + 1), cpar);
       }
@@ -813,6 +851,7 @@ __global__ void __launch_bounds__(BLOCK) scatter_kernel(Ws ws, int L) {
     BS_PROBE(6);
     cur ^= 1;
   }
+  BS_PROBE_FLUSH();
 }
 
 // ---------------------------------------------------------------------------
@@ -893,7 +932,7 @@ __global__ void __launch_bounds__(BLOCK + 32) scatter_ws_kernel(Ws ws, int L) {
     if (lane != 0) return;
     for (uint32_t i = 0;; ++i) {
       const int s = int(i % NBUF);
-      if (i >= NBUF) mbar_wait(&empty[s], ((i / NBUF) - 1) & 1u);
+      if (i >= NBUF) mbar_wait_sleep(&empty[s], ((i / NBUF) - 1) & 1u);
       InFlight f{};
       f.idx = atomicAdd(&ws.ctl->ticket[L], 1u);
       if (f.idx < nt) {
@@ -993,6 +1032,253 @@ __global__ void __launch_bounds__(BLOCK + 32) scatter_ws_kernel(Ws ws, int L) {
     named_sync<BLOCK>();  // every consumer is done with buffer s
     if (tid == 0) mbar_arrive(&empty[s]);
   }
+}
+
+// ---------------------------------------------------------------------------
+// K4a: dense keys-only local sort (the common case after two 8-bit MSD levels
+// of full-width keys: each task's keys differ only inside a 16-bit span).
+// Counting sort through per-task bitmaps, warp-specialised like the scatter:
+// a producer warp streams tasks in by TMA into a two-slot ring while BLOCK
+// consumer threads sort the previous one.
+//   insert:  one shared atomicOr per key into B1 (first copy) / B2 (second
+//            copy); later copies go to a small overflow list (flag in word);
+//   scan:    per-word copy counts -> exclusive word prefix WP;
+//   place:   pos = WP + popc(B1 & below) + popc(B2 & below) + copy index.
+// The keys stay in registers, so the consumed input slot is the staging
+// buffer and the output is written coalesced.  A task with more repeats than
+// the overflow list holds is handed to the general local sort.
+// ---------------------------------------------------------------------------
+template <typename K, int BLOCK, int KPT, int NSLOT>
+struct DenseSmem {
+  static constexpr int CAP = BLOCK * KPT;
+  static constexpr int NW = 2048;      // 2^16 values / 32
+  static constexpr int DUPCAP = 1024;  // third+ copies
+  static constexpr size_t kbuf = (sizeof(K) * CAP + 32 + 15) & ~size_t(15);
+  static constexpr size_t dbuf_off = 0;
+  static constexpr size_t stg_off = dbuf_off + NSLOT * kbuf;  // staging (sorted task)
+  // structure-of-arrays bitmaps: random words spread over all 32 banks
+  static constexpr size_t b1_off = stg_off + kbuf;
+  static constexpr size_t b2_off = b1_off + sizeof(uint32_t) * NW;
+  static constexpr size_t wp_off = b2_off + sizeof(uint32_t) * NW;  // extra-copy count -> WP | flag
+  static constexpr size_t cp_off = wp_off + sizeof(uint32_t) * NW;  // copy index of repeated keys
+  static constexpr size_t dup_off = cp_off + sizeof(uint16_t) * CAP;
+  static constexpr size_t misc_off = (dup_off + sizeof(uint32_t) * DUPCAP + 15) & ~size_t(15);
+  static constexpr size_t bars_off = misc_off + sizeof(uint32_t) * 64;
+  static constexpr size_t info_off = bars_off + sizeof(uint64_t) * 2 * NSLOT;
+  static constexpr size_t bytes = info_off + sizeof(InFlight) * NSLOT;
+};
+
+template <typename K, int KIND, int BLOCK, int KPT, int NSLOT>
+__global__ void __launch_bounds__(BLOCK + 32) dense_kernel(Ws ws) {
+  using S = DenseSmem<K, BLOCK, KPT, NSLOT>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  K *stg = reinterpret_cast<K *>(smem + S::stg_off);
+  uint32_t *B1 = reinterpret_cast<uint32_t *>(smem + S::b1_off);
+  uint32_t *B2 = reinterpret_cast<uint32_t *>(smem + S::b2_off);
+  uint32_t *WP = reinterpret_cast<uint32_t *>(smem + S::wp_off);
+  uint16_t *cpv = reinterpret_cast<uint16_t *>(smem + S::cp_off);
+  uint32_t *dup = reinterpret_cast<uint32_t *>(smem + S::dup_off);
+  uint32_t *misc = reinterpret_cast<uint32_t *>(smem + S::misc_off);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + S::bars_off);
+  uint64_t *empty = full + NSLOT;
+  InFlight *info = reinterpret_cast<InFlight *>(smem + S::info_off);
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const uint32_t nt = min(ws.ctl->ndtasks, ws.maxtasks);
+  if (blockIdx.x >= nt) return;
+  const KeyGeom<K, KIND> g{0};
+  if (tid == BLOCK) {
+    for (int i = 0; i < NSLOT; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (w == BLOCK / 32) {  // ---------------- producer warp ----------------
+    if (lane != 0) return;
+    uint32_t ti = blockIdx.x;
+    DTask nxt = ws.dtasks[ti];  // task records are fetched one task ahead
+    for (uint32_t i = 0;; ++i) {
+      const int s = int(i % NSLOT);
+      const DTask t = nxt;
+      const uint32_t tn = ti + gridDim.x;
+      if (tn < nt) nxt = ws.dtasks[tn];
+      if (i >= NSLOT) mbar_wait_sleep(&empty[s], ((i / NSLOT) - 1) & 1u);
+      InFlight f{};
+      f.idx = ti;
+      if (ti < nt) {
+        f.start = t.start;
+        f.cnt = t.count;
+        f.digit = t.meta;  // lb | span << 8 | parity << 16
+        f.parity = t.meta >> 16;
+        const Span sk = span16(static_cast<const K *>(ws.keys[f.parity]) + f.start, f.cnt);
+        f.headk = sk.head;
+        info[s] = f;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&full[s], sk.bytes);
+        bulk_g2s(smem + S::dbuf_off + s * S::kbuf, sk.base, sk.bytes, &full[s]);
+      } else {
+        info[s] = f;
+        mbar_arrive(&full[s]);
+        return;
+      }
+      ti = tn;
+    }
+  }
+
+  // ---------------- consumers ----------------
+  BS_PROBE_INIT();
+  for (uint32_t i = 0;; ++i) {
+    const int s = int(i % NSLOT);
+    BS_PROBE(8);
+    mbar_wait(&full[s], (i / NSLOT) & 1u);
+    BS_PROBE(9);
+    const InFlight f = info[s];
+    if (f.idx >= nt) break;
+    const K *kb = reinterpret_cast<const K *>(smem + S::dbuf_off + s * S::kbuf) + f.headk;
+    const int n = int(f.cnt);
+    const int lb = int(f.digit & 0xFFu), span = int((f.digit >> 8) & 0xFFu);
+    const uint32_t vmask = (span >= 32) ? 0xFFFFFFFFu : ((1u << span) - 1u);
+    // bitmap words, rounded up to 8 per thread-chunk (vectorised zero/scan)
+    const int nw = span <= 8 ? 8 : (1 << (span - 5));
+    for (int q = tid; q < nw / 4; q += BLOCK) {
+      reinterpret_cast<uint4 *>(B1)[q] = make_uint4(0, 0, 0, 0);
+      reinterpret_cast<uint4 *>(B2)[q] = make_uint4(0, 0, 0, 0);
+      reinterpret_cast<uint4 *>(WP)[q] = make_uint4(0, 0, 0, 0);
+    }
+    if (tid == 0) misc[32] = 0;  // overflow count
+    named_sync<BLOCK>();
+    BS_PROBE(10);
+    // presence atomics; a key that finds its bit set is a repeat
+    uint32_t rep = 0;  // bit j: key j is not the first copy of its value
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+      const int e = j * BLOCK + tid;
+      if (e < n) {
+        const uint32_t idx = uint32_t(g.norm(kb[e]) >> lb) & vmask;
+        const uint32_t bit = 1u << (idx & 31u);
+        if (atomicOr(&B1[idx >> 5], bit) & bit) rep |= 1u << j;
+      }
+    }
+    if (rep) {  // rare per thread: second copies -> B2, later ones -> overflow list
+#pragma unroll
+      for (int j = 0; j < KPT; ++j) {
+        if ((rep >> j) & 1u) {
+          const int e = j * BLOCK + tid;
+          const uint32_t idx = uint32_t(g.norm(kb[e]) >> lb) & vmask;
+          const uint32_t bit = 1u << (idx & 31u);
+          uint32_t c = 1;
+          if (atomicOr(&B2[idx >> 5], bit) & bit) {
+            atomicAdd(&WP[idx >> 5], 1u);
+            const uint32_t sl = atomicAdd(&misc[32], 1u);
+            if (sl < S::DUPCAP) dup[sl] = idx;
+            c = 2 + min(sl, uint32_t(S::DUPCAP));
+          }
+          cpv[e] = uint16_t(c);
+        }
+      }
+    }
+    named_sync<BLOCK>();
+    BS_PROBE(11);
+    const uint32_t ndup = misc[32];
+    if (ndup > S::DUPCAP) {
+      // too many repeats: hand the task to the general local sort
+      if (tid == 0) emit_tasks(ws, f.start, f.cnt, f.parity);
+      named_sync<BLOCK>();
+      if (tid == 0) mbar_arrive(&empty[s]);
+      continue;
+    }
+    {
+      // Word prefix WP (copies of all smaller values): thread-contiguous runs
+      // of 8 words, read and written as uint4.
+      const int q0 = tid * 8;
+      uint32_t cw[8];
+      uint32_t c = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) cw[k] = 0;
+      if (q0 < nw) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint4 b1 = reinterpret_cast<const uint4 *>(B1)[(q0 >> 2) + h];
+          const uint4 b2 = reinterpret_cast<const uint4 *>(B2)[(q0 >> 2) + h];
+          const uint4 ex = reinterpret_cast<const uint4 *>(WP)[(q0 >> 2) + h];
+          cw[4 * h + 0] = (__popc(b1.x) + __popc(b2.x) + ex.x) | (ex.x ? 0x80000000u : 0u);
+          cw[4 * h + 1] = (__popc(b1.y) + __popc(b2.y) + ex.y) | (ex.y ? 0x80000000u : 0u);
+          cw[4 * h + 2] = (__popc(b1.z) + __popc(b2.z) + ex.z) | (ex.z ? 0x80000000u : 0u);
+          cw[4 * h + 3] = (__popc(b1.w) + __popc(b2.w) + ex.w) | (ex.w ? 0x80000000u : 0u);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) c += cw[k] & 0x7FFFFFFFu;
+      }
+      uint32_t incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) misc[w] = incl;
+      named_sync<BLOCK>();
+      if (w == 0) {
+        const uint32_t sv = (lane < BLOCK / 32) ? misc[lane] : 0u;
+        uint32_t si = sv;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, si, o);
+          if (lane >= o) si += y;
+        }
+        if (lane < BLOCK / 32) misc[lane] = si - sv;
+      }
+      named_sync<BLOCK>();
+      if (q0 < nw) {
+        uint32_t run = misc[w] + incl - c;
+        uint32_t o8[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          o8[k] = run | (cw[k] & 0x80000000u);
+          run += cw[k] & 0x7FFFFFFFu;
+        }
+        reinterpret_cast<uint4 *>(WP)[(q0 >> 2)] = make_uint4(o8[0], o8[1], o8[2], o8[3]);
+        reinterpret_cast<uint4 *>(WP)[(q0 >> 2) + 1] = make_uint4(o8[4], o8[5], o8[6], o8[7]);
+      }
+    }
+    named_sync<BLOCK>();
+    BS_PROBE(12);
+    // place: copies of smaller values + copy index
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+      const int e = j * BLOCK + tid;
+      if (e < n) {
+        const K x = kb[e];
+        const uint32_t idx = uint32_t(g.norm(x) >> lb) & vmask;
+        const uint32_t q = idx >> 5;
+        const uint32_t below = (1u << (idx & 31u)) - 1u;
+        const uint32_t wp = WP[q];
+        uint32_t p = (wp & 0x7FFFFFFFu) + __popc(B1[q] & below) + __popc(B2[q] & below);
+        if (((rep >> j) & 1u) | (wp >> 31)) {  // repeats in play
+          const uint32_t c = ((rep >> j) & 1u) ? cpv[e] : 0u;
+          if (wp >> 31) {
+            for (uint32_t t = 0; t < ndup; ++t) {
+              const uint32_t o = dup[t];
+              p += ((o >> 5) == q && o < idx) ? 1u : 0u;
+              p += (c >= 2 && o == idx && t < c - 2) ? 1u : 0u;
+            }
+          }
+          p += c < 2 ? c : 2u;
+        }
+        stg[p] = x;
+      }
+    }
+    named_sync<BLOCK>();
+    BS_PROBE(13);
+    // the input slot is free once every key is staged: release it early
+    if (tid == 0) mbar_arrive(&empty[s]);
+    K *dst = static_cast<K *>(ws.keys[0]) + f.start;
+    for (int e = tid; e < n; e += BLOCK) __stcs(dst + e, stg[e]);
+    named_sync<BLOCK>();
+    BS_PROBE(14);
+  }
+  BS_PROBE_FLUSH();
 }
 
 // ---------------------------------------------------------------------------
