@@ -272,6 +272,9 @@ def binar_sort_range(seq, rng: SortRange, codec, metrics: Metrics, observer=None
 
 def _sort_device(seq, codec, values, width, start_pos, depth, metrics, lower=0, upper=None,
                  with_metrics=True):
+    if codec.gpu_spec(seq) is None:  # generic-engine element types: out of scope
+        raise TypeError(f"{type(codec).__name__} on {type(seq).__name__} has no word view "
+                        "(the B200 backend sorts 1-D integer/float arrays, tensors and lists)")
     t = device.require_cuda()
     w = DeviceWords(seq, codec, values, lower=lower, upper=upper)
     counters = t.zeros(4, dtype=t.int64, device=w.keys.device) if with_metrics else None

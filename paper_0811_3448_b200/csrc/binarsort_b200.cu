@@ -277,14 +277,14 @@ int bs_sort(void *keys, void *vals, uint64_t n, int key_bytes, int val_bytes, in
             int key_kind, void *ws, size_t ws_bytes, void *stream, int64_t *counters, int64_t depth) {
   int rc = check_common(key_bytes, val_bytes, width, start_pos, key_kind);
   if (rc) return rc;
-  if (val_bytes != 0 && vals == nullptr) return fail(BS_ERR_VALUE, "val_bytes > 0 but vals is NULL");
   if (n >= (uint64_t(1) << 30) + 1) return fail(BS_ERR_VALUE, "n > 2^30 elements per call is not supported");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int width_eff = width - start_pos;
   // the sign bit lies above the effective key once start_pos > 0
   if (key_kind == BS_KEY_SIGNED && start_pos > 0) key_kind = BS_KEY_UNSIGNED;
   if (counters) BS_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(int64_t), st));
-  if (n <= 1 || width_eff == 0) return BS_OK;
+  if (n <= 1 || width_eff == 0) return BS_OK;  // nothing to move (core.py:207-212)
+  if (val_bytes != 0 && vals == nullptr) return fail(BS_ERR_VALUE, "val_bytes > 0 but vals is NULL");
   if (val_bytes == 0) vals = nullptr;
 #define BS_DISPATCH_V(K, KIND)                                                                  \
   do {                                                                                          \
