@@ -175,14 +175,20 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   constexpr bool WSPEC = VB == 0;  // keys-only: warp-specialised scatter
   auto sc = scatter_kernel<K, VB, KIND, SC_BLOCK, SKPT>;
   auto sw = scatter_ws_kernel<K, KIND, SC_BLOCK, SKPT, SC_NBUF>;
-  // dense local sort: 512 consumers x 12 keys (6144-key tasks), 2-slot ring
-  constexpr int DN_BLOCK = 512, DN_KPT = 12, DN_SLOTS = 2;
+  // dense local sort: 512 consumers x 11 keys (5632-key tasks), 2-slot ring;
+  // big variant (u32 only) 512 x 36 (18432-key tasks, e.g. 2^30-key inputs),
+  // single slot
+  constexpr int DN_BLOCK = 512, DN_KPT = 11, DN_SLOTS = 2;
+  constexpr int DB_KPT = sizeof(K) == 4 ? 36 : 12;
   using DS = DenseSmem<K, DN_BLOCK, DN_KPT, DN_SLOTS>;
-  auto dk = dense_kernel<K, KIND, DN_BLOCK, DN_KPT, DN_SLOTS>;
+  using DB = DenseSmem<K, DN_BLOCK, DB_KPT, 1>;
+  auto dk = dense_kernel<K, KIND, DN_BLOCK, DN_KPT, DN_SLOTS, false>;
+  auto db = dense_kernel<K, KIND, DN_BLOCK, DB_KPT, 1, true>;
   ws.dense_max = DN_BLOCK * DN_KPT;
+  ws.dense_big_max = sizeof(K) == 4 ? DN_BLOCK * DB_KPT : 0;
   auto lc = local_kernel<K, VB, KIND, LC_BLOCK, LC_KPT>;
   auto hk = hist_kernel<K, KIND, HI_BLOCK, HKPT>;
-  static int sc_grid = 0, lc_grid = 0, hk_grid = 0, dk_grid = 0;
+  static int sc_grid = 0, lc_grid = 0, hk_grid = 0, dk_grid = 0, db_grid = 0;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
@@ -191,6 +197,9 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
     cudaError_t e3 = cudaFuncSetAttribute(sw, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SW::bytes));
     cudaError_t e4 = VB == 0 ? cudaFuncSetAttribute(dk, cudaFuncAttributeMaxDynamicSharedMemorySize, int(DS::bytes))
                              : cudaSuccess;
+    if (VB == 0 && e4 == cudaSuccess)
+      e4 = cudaFuncSetAttribute(db, cudaFuncAttributeMaxDynamicSharedMemorySize, int(DB::bytes));
+    db_grid = VB == 0 ? num_sms() * max_active(db, DN_BLOCK + 32, DB::bytes) : 0;
     attr_err = e1 != cudaSuccess ? e1 : (e2 != cudaSuccess ? e2 : (e3 != cudaSuccess ? e3 : e4));
     dk_grid = VB == 0 ? num_sms() * max_active(dk, DN_BLOCK + 32, DS::bytes) : 0;
     sc_grid = WSPEC ? num_sms() * max_active(sw, SC_BLOCK + 32, SW::bytes)
@@ -214,15 +223,19 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
       hk<<<hk_grid, HI_BLOCK, 0, st>>>(ws, L);
       mark(st);
       plan_kernel<K><<<num_sms() * 4, 256, 0, st>>>(ws, L);
-      expand_kernel<<<num_sms() * 4, 256, 0, st>>>(ws, L + 1);
       mark(st);
       if constexpr (WSPEC) sw<<<sc_grid, SC_BLOCK + 32, SW::bytes, st>>>(ws, L);
       else sc<<<sc_grid, SC_BLOCK, SS::bytes, st>>>(ws, L);
+      if constexpr (VB == 0) {
+        // big dense children of this level (their data is in place now)
+        if (ws.dense && ws.dense_big_max && L < nlev - 1) db<<<db_grid, DN_BLOCK + 32, DB::bytes, st>>>(ws, L);
+      }
+      expand_kernel<<<num_sms() * 4, 256, 0, st>>>(ws, L + 1);
       mark(st);
     }
   }
   if constexpr (VB == 0) {
-    if (ws.dense) dk<<<dk_grid, DN_BLOCK + 32, DS::bytes, st>>>(ws);
+    if (ws.dense) dk<<<dk_grid, DN_BLOCK + 32, DS::bytes, st>>>(ws, 0);
   }
   lc<<<lc_grid, LC_BLOCK, LS::bytes, st>>>(ws);
   mark(st);
@@ -336,7 +349,7 @@ int bs_sort_launches(uint64_t n, int key_bytes, int width, int start_pos, int wi
   if (n <= 1 || width_eff <= 0) return 0;
   const Geometry g = geometry(n, key_bytes, 0, width_eff);
   int k = 3;  // init + dense + local
-  if (n > g.local_max) k += 4 * (g.ndig + 1);
+  if (n > g.local_max) k += 4 * (g.ndig + 1) + (key_bytes == 4 ? g.ndig : 0);  // + big dense per level
   if (with_counters) k += 2;
   return k;
 }

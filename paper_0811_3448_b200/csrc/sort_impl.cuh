@@ -18,6 +18,8 @@
 // then K4 local_kernel over the task list.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace bs {
@@ -77,7 +79,7 @@ struct DTask {
   uint64_t start;
   uint64_t common;
   uint32_t count;
-  uint32_t meta;  // lb | span << 8 | parity << 16
+  uint32_t meta;  // lb | span << 8 | parity << 16 | digit << 20 (digit: big tasks' next MSD digit)
 };
 
 struct Ctl {
@@ -85,9 +87,10 @@ struct Ctl {
   uint32_t ntiles[MAXLEV + 1];
   uint32_t ticket[MAXLEV + 1];
   uint32_t ntasks;
-  uint32_t ndtasks;
-  uint32_t error;  // bit 0: bucket overflow, 1: tile overflow, 2: task overflow
-  uint32_t pad;
+  uint32_t ndtasks;      // small dense tasks (front of dtasks)
+  uint32_t error;        // bit 0: bucket overflow, 1: tile overflow, 2: task overflow
+  uint32_t ndtasks_big;  // big dense tasks (back of dtasks)
+  uint32_t dbig_end[MAXLEV + 1];  // ndtasks_big after plan(L) (snapshot by scatter(L))
 };
 
 // Workspace view (all device pointers), built on the host.
@@ -102,7 +105,8 @@ struct Ws {
   Task *tasks;
   DTask *dtasks;
   int dense;           // keys-only full-width: dense tasks go to dense_kernel
-  uint32_t dense_max;  // dense_kernel capacity
+  uint32_t dense_max;      // small dense_kernel capacity
+  uint32_t dense_big_max;  // big dense_kernel capacity (0: none)
   void *keys[2];  // [0] caller's buffer, [1] workspace copy
   void *vals[2];
   uint64_t n;
@@ -348,6 +352,15 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
       __syncthreads();
       continue;
     }
+    // standalone children whose varying bits fit a 16-bit span are dense tasks
+    const int lbv = __ffsll((long long)uint64_t(lower)) - 1;
+    const int spanv = W - KeyTraits<K>::clz(lower) - lbv;
+    const bool dense = ws.dense && spanv <= 16;
+    // dense children up to the big dense kernel's capacity stay local even
+    // when they exceed local_max (no further global level for them)
+    // (big ones only while dense enough that repeats stay rare: n <= 2^span / 3.5)
+    const uint32_t big_max =
+        dense ? max(ws.local_max, min(ws.dense_big_max, uint32_t((2ull << spanv) / 7))) : ws.local_max;
     __syncthreads();
     if (tid == 0) {
       // greedy in digit order: large children go to the next level, mid-size
@@ -362,7 +375,7 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
         if (cd >= ws.group_min) {
           if (gc) s_emit[ne++] = Emit{gs, gc, 1, 0xFFFFFFFFu};
           gc = 0;
-          s_emit[ne++] = Emit{pos, cd, cd > ws.local_max ? 0u : 1u, uint32_t(d)};
+          s_emit[ne++] = Emit{pos, cd, cd > big_max ? 0u : 1u, uint32_t(d)};
         } else {
           if (gc + cd > ws.local_max) {
             s_emit[ne++] = Emit{gs, gc, 1, 0xFFFFFFFFu};
@@ -378,10 +391,6 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
     }
     __syncthreads();
     const uint32_t ne = s_nemit;
-    // standalone children whose varying bits fit a 16-bit span are dense tasks
-    const int lbv = __ffsll((long long)uint64_t(lower)) - 1;
-    const int spanv = W - KeyTraits<K>::clz(lower) - lbv;
-    const bool dense = ws.dense && spanv <= 16;
     const K spanmask = (spanv >= W ? ~K(0) : ((K(1) << spanv) - 1)) << lbv;
     const K dmask = K(0xFF) << lowbits;
     const K cbase = K(ws.bor[cur][b]) & ~spanmask & ~dmask;
@@ -389,13 +398,18 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
       const Emit e = s_emit[i];
       if (e.kind == 1) {
         if (e.count == 1 && cpar == 0) continue;  // singleton already home: done
-        if (dense && e.digit != 0xFFFFFFFFu && e.count > 1 && e.count <= ws.dense_max) {
-          const uint32_t slot = atomicAdd(&ws.ctl->ndtasks, 1u);
-          if (slot < ws.maxtasks)
+        if (dense && e.digit != 0xFFFFFFFFu && e.count > 1 && e.count <= big_max) {
+          // small dense tasks fill the list from the front, big ones from the back
+          const bool big = e.count > ws.dense_max;
+          const uint32_t k = atomicAdd(big ? &ws.ctl->ndtasks_big : &ws.ctl->ndtasks, 1u);
+          if (k < ws.maxtasks / 2) {
+            const uint32_t slot = big ? ws.maxtasks - 1 - k : k;
             ws.dtasks[slot] = DTask{e.start, uint64_t(cbase | (K(e.digit) << lowbits)), e.count,
-                                    uint32_t(lbv) | (uint32_t(spanv) << 8) | (cpar << 16)};
-          else
+                                    uint32_t(lbv) | (uint32_t(spanv) << 8) | (cpar << 16) |
+                                        (uint32_t(dig + 1) << 20)};
+          } else {
             atomicOr(&ws.ctl->error, 4u);
+          }
         } else {
           emit_tasks(ws, e.start, e.count, cpar);
         }
@@ -918,6 +932,8 @@ __global__ void __launch_bounds__(BLOCK + 32) scatter_ws_kernel(Ws ws, int L) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int lv = L & 1;
   const uint32_t nt = ws.ctl->ntiles[L];
+  // plan(L) is complete: snapshot the big dense tasks it created
+  if (blockIdx.x == 0 && tid == 0) ws.ctl->dbig_end[L] = ws.ctl->ndtasks_big;
   if (nt == 0) return;
   if (tid == BLOCK) {
     for (int i = 0; i < NBUF; ++i) {
@@ -1052,14 +1068,15 @@ template <typename K, int BLOCK, int KPT, int NSLOT>
 struct DenseSmem {
   static constexpr int CAP = BLOCK * KPT;
   static constexpr int NW = 2048;      // 2^16 values / 32
-  static constexpr int DUPCAP = 1024;  // third+ copies
+  static constexpr int DUPCAP = CAP > 8192 ? 1024 : 256;  // fourth+ copies
   static constexpr size_t kbuf = (sizeof(K) * CAP + 32 + 15) & ~size_t(15);
   static constexpr size_t dbuf_off = 0;
   static constexpr size_t stg_off = dbuf_off + NSLOT * kbuf;  // staging (sorted task)
   // structure-of-arrays bitmaps: random words spread over all 32 banks
   static constexpr size_t b1_off = stg_off + kbuf;
   static constexpr size_t b2_off = b1_off + sizeof(uint32_t) * NW;
-  static constexpr size_t wp_off = b2_off + sizeof(uint32_t) * NW;  // extra-copy count -> WP | flag
+  static constexpr size_t b3_off = b2_off + sizeof(uint32_t) * NW;
+  static constexpr size_t wp_off = b3_off + sizeof(uint32_t) * NW;  // extra-copy count -> WP | flags
   static constexpr size_t cp_off = wp_off + sizeof(uint32_t) * NW;  // copy index of repeated keys
   static constexpr size_t dup_off = cp_off + sizeof(uint16_t) * CAP;
   static constexpr size_t misc_off = (dup_off + sizeof(uint32_t) * DUPCAP + 15) & ~size_t(15);
@@ -1068,13 +1085,14 @@ struct DenseSmem {
   static constexpr size_t bytes = info_off + sizeof(InFlight) * NSLOT;
 };
 
-template <typename K, int KIND, int BLOCK, int KPT, int NSLOT>
-__global__ void __launch_bounds__(BLOCK + 32) dense_kernel(Ws ws) {
+template <typename K, int KIND, int BLOCK, int KPT, int NSLOT, bool BIG>
+__global__ void __launch_bounds__(BLOCK + 32) dense_kernel(Ws ws, int L) {
   using S = DenseSmem<K, BLOCK, KPT, NSLOT>;
   extern __shared__ __align__(128) unsigned char smem[];
   K *stg = reinterpret_cast<K *>(smem + S::stg_off);
   uint32_t *B1 = reinterpret_cast<uint32_t *>(smem + S::b1_off);
   uint32_t *B2 = reinterpret_cast<uint32_t *>(smem + S::b2_off);
+  uint32_t *B3 = reinterpret_cast<uint32_t *>(smem + S::b3_off);
   uint32_t *WP = reinterpret_cast<uint32_t *>(smem + S::wp_off);
   uint16_t *cpv = reinterpret_cast<uint16_t *>(smem + S::cp_off);
   uint32_t *dup = reinterpret_cast<uint32_t *>(smem + S::dup_off);
@@ -1083,8 +1101,16 @@ __global__ void __launch_bounds__(BLOCK + 32) dense_kernel(Ws ws) {
   uint64_t *empty = full + NSLOT;
   InFlight *info = reinterpret_cast<InFlight *>(smem + S::info_off);
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  const uint32_t nt = min(ws.ctl->ndtasks, ws.maxtasks);
+  // Small dense tasks: the whole list, after all levels.  Big ones: the tasks
+  // planned at level L, right after scatter(L), so one that overflows can
+  // still be pushed to level L+1 as an ordinary bucket.
+  const uint32_t k0 = BIG ? (L > 0 ? ws.ctl->dbig_end[L - 1] : 0u) : 0u;
+  const uint32_t nt = min(BIG ? ws.ctl->dbig_end[L] : ws.ctl->ndtasks, ws.maxtasks / 2) - min(k0, ws.maxtasks / 2);
   if (blockIdx.x >= nt) return;
+  // big tasks are stored from the back of the list
+  auto task_at = [&](uint32_t k) -> const DTask & {
+    return ws.dtasks[BIG ? ws.maxtasks - 1 - (k0 + k) : k];
+  };
   const KeyGeom<K, KIND> g{0};
   if (tid == BLOCK) {
     for (int i = 0; i < NSLOT; ++i) {
@@ -1098,20 +1124,20 @@ __global__ void __launch_bounds__(BLOCK + 32) dense_kernel(Ws ws) {
   if (w == BLOCK / 32) {  // ---------------- producer warp ----------------
     if (lane != 0) return;
     uint32_t ti = blockIdx.x;
-    DTask nxt = ws.dtasks[ti];  // task records are fetched one task ahead
+    DTask nxt = task_at(ti);  // task records are fetched one task ahead
     for (uint32_t i = 0;; ++i) {
       const int s = int(i % NSLOT);
       const DTask t = nxt;
       const uint32_t tn = ti + gridDim.x;
-      if (tn < nt) nxt = ws.dtasks[tn];
+      if (tn < nt) nxt = task_at(tn);
       if (i >= NSLOT) mbar_wait_sleep(&empty[s], ((i / NSLOT) - 1) & 1u);
       InFlight f{};
       f.idx = ti;
       if (ti < nt) {
         f.start = t.start;
         f.cnt = t.count;
-        f.digit = t.meta;  // lb | span << 8 | parity << 16
-        f.parity = t.meta >> 16;
+        f.digit = t.meta;  // lb | span << 8 | parity << 16 | digit << 20
+        f.parity = (t.meta >> 16) & 1u;
         const Span sk = span16(static_cast<const K *>(ws.keys[f.parity]) + f.start, f.cnt);
         f.headk = sk.head;
         info[s] = f;
@@ -1145,35 +1171,40 @@ __global__ void __launch_bounds__(BLOCK + 32) dense_kernel(Ws ws) {
     for (int q = tid; q < nw / 4; q += BLOCK) {
       reinterpret_cast<uint4 *>(B1)[q] = make_uint4(0, 0, 0, 0);
       reinterpret_cast<uint4 *>(B2)[q] = make_uint4(0, 0, 0, 0);
+      reinterpret_cast<uint4 *>(B3)[q] = make_uint4(0, 0, 0, 0);
       reinterpret_cast<uint4 *>(WP)[q] = make_uint4(0, 0, 0, 0);
     }
     if (tid == 0) misc[32] = 0;  // overflow count
     named_sync<BLOCK>();
     BS_PROBE(10);
     // presence atomics; a key that finds its bit set is a repeat
-    uint32_t rep = 0;  // bit j: key j is not the first copy of its value
+    using Mask = typename std::conditional<(KPT > 32), unsigned long long, uint32_t>::type;
+    Mask rep = 0;  // bit j: key j is not the first copy of its value
 #pragma unroll
     for (int j = 0; j < KPT; ++j) {
       const int e = j * BLOCK + tid;
       if (e < n) {
         const uint32_t idx = uint32_t(g.norm(kb[e]) >> lb) & vmask;
         const uint32_t bit = 1u << (idx & 31u);
-        if (atomicOr(&B1[idx >> 5], bit) & bit) rep |= 1u << j;
+        if (atomicOr(&B1[idx >> 5], bit) & bit) rep |= Mask(1) << j;
       }
     }
     if (rep) {  // rare per thread: second copies -> B2, later ones -> overflow list
 #pragma unroll
       for (int j = 0; j < KPT; ++j) {
-        if ((rep >> j) & 1u) {
+        if ((rep >> j) & Mask(1)) {
           const int e = j * BLOCK + tid;
           const uint32_t idx = uint32_t(g.norm(kb[e]) >> lb) & vmask;
           const uint32_t bit = 1u << (idx & 31u);
           uint32_t c = 1;
           if (atomicOr(&B2[idx >> 5], bit) & bit) {
-            atomicAdd(&WP[idx >> 5], 1u);
-            const uint32_t sl = atomicAdd(&misc[32], 1u);
-            if (sl < S::DUPCAP) dup[sl] = idx;
-            c = 2 + min(sl, uint32_t(S::DUPCAP));
+            c = 2;
+            if (atomicOr(&B3[idx >> 5], bit) & bit) {  // fourth+ copies: overflow list
+              atomicAdd(&WP[idx >> 5], 1u);
+              const uint32_t sl = atomicAdd(&misc[32], 1u);
+              if (sl < S::DUPCAP) dup[sl] = idx;
+              c = 3 + min(sl, uint32_t(S::DUPCAP));
+            }
           }
           cpv[e] = uint16_t(c);
         }
@@ -1183,8 +1214,12 @@ __global__ void __launch_bounds__(BLOCK + 32) dense_kernel(Ws ws) {
     BS_PROBE(11);
     const uint32_t ndup = misc[32];
     if (ndup > S::DUPCAP) {
-      // too many repeats: hand the task to the general local sort
-      if (tid == 0) emit_tasks(ws, f.start, f.cnt, f.parity);
+      // too many repeats: hand the task to the general local sort (small) or
+      // to the next MSD level as an ordinary bucket (big)
+      if (tid == 0) {
+        if (BIG) push_bucket(ws, L, f.start, f.cnt, (f.digit >> 20) & 0xFu, f.parity & 1u);
+        else emit_tasks(ws, f.start, f.cnt, f.parity & 1u);
+      }
       named_sync<BLOCK>();
       if (tid == 0) mbar_arrive(&empty[s]);
       continue;
@@ -1202,14 +1237,20 @@ __global__ void __launch_bounds__(BLOCK + 32) dense_kernel(Ws ws) {
         for (int h = 0; h < 2; ++h) {
           const uint4 b1 = reinterpret_cast<const uint4 *>(B1)[(q0 >> 2) + h];
           const uint4 b2 = reinterpret_cast<const uint4 *>(B2)[(q0 >> 2) + h];
+          const uint4 b3 = reinterpret_cast<const uint4 *>(B3)[(q0 >> 2) + h];
           const uint4 ex = reinterpret_cast<const uint4 *>(WP)[(q0 >> 2) + h];
-          cw[4 * h + 0] = (__popc(b1.x) + __popc(b2.x) + ex.x) | (ex.x ? 0x80000000u : 0u);
-          cw[4 * h + 1] = (__popc(b1.y) + __popc(b2.y) + ex.y) | (ex.y ? 0x80000000u : 0u);
-          cw[4 * h + 2] = (__popc(b1.z) + __popc(b2.z) + ex.z) | (ex.z ? 0x80000000u : 0u);
-          cw[4 * h + 3] = (__popc(b1.w) + __popc(b2.w) + ex.w) | (ex.w ? 0x80000000u : 0u);
+          // WP flags: bit 31 overflow list, bit 30 second copies, bit 29 third copies
+          auto cnt = [](uint32_t x1, uint32_t x2, uint32_t x3, uint32_t e) {
+            return (__popc(x1) + __popc(x2) + __popc(x3) + e) | (e ? 0x80000000u : 0u) |
+                   (x2 ? 0x40000000u : 0u) | (x3 ? 0x20000000u : 0u);
+          };
+          cw[4 * h + 0] = cnt(b1.x, b2.x, b3.x, ex.x);
+          cw[4 * h + 1] = cnt(b1.y, b2.y, b3.y, ex.y);
+          cw[4 * h + 2] = cnt(b1.z, b2.z, b3.z, ex.z);
+          cw[4 * h + 3] = cnt(b1.w, b2.w, b3.w, ex.w);
         }
 #pragma unroll
-        for (int k = 0; k < 8; ++k) c += cw[k] & 0x7FFFFFFFu;
+        for (int k = 0; k < 8; ++k) c += cw[k] & 0x1FFFFFFFu;
       }
       uint32_t incl = c;
 #pragma unroll
@@ -1235,8 +1276,8 @@ __global__ void __launch_bounds__(BLOCK + 32) dense_kernel(Ws ws) {
         uint32_t o8[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          o8[k] = run | (cw[k] & 0x80000000u);
-          run += cw[k] & 0x7FFFFFFFu;
+          o8[k] = run | (cw[k] & 0xE0000000u);
+          run += cw[k] & 0x1FFFFFFFu;
         }
         reinterpret_cast<uint4 *>(WP)[(q0 >> 2)] = make_uint4(o8[0], o8[1], o8[2], o8[3]);
         reinterpret_cast<uint4 *>(WP)[(q0 >> 2) + 1] = make_uint4(o8[4], o8[5], o8[6], o8[7]);
@@ -1254,17 +1295,20 @@ __global__ void __launch_bounds__(BLOCK + 32) dense_kernel(Ws ws) {
         const uint32_t q = idx >> 5;
         const uint32_t below = (1u << (idx & 31u)) - 1u;
         const uint32_t wp = WP[q];
-        uint32_t p = (wp & 0x7FFFFFFFu) + __popc(B1[q] & below) + __popc(B2[q] & below);
-        if (((rep >> j) & 1u) | (wp >> 31)) {  // repeats in play
-          const uint32_t c = ((rep >> j) & 1u) ? cpv[e] : 0u;
-          if (wp >> 31) {
+        uint32_t p = (wp & 0x1FFFFFFFu) + __popc(B1[q] & below);
+        if (wp & 0x40000000u) p += __popc(B2[q] & below);
+        if (wp & 0x20000000u) p += __popc(B3[q] & below);
+        const bool isrep = (rep >> j) & Mask(1);
+        if (isrep || (wp >> 31)) {  // repeats in play
+          const uint32_t c = isrep ? cpv[e] : 0u;
+          if (wp >> 31) {  // rare: fourth+ copies listed for this word
             for (uint32_t t = 0; t < ndup; ++t) {
               const uint32_t o = dup[t];
               p += ((o >> 5) == q && o < idx) ? 1u : 0u;
-              p += (c >= 2 && o == idx && t < c - 2) ? 1u : 0u;
+              p += (c >= 3 && o == idx && t < c - 3) ? 1u : 0u;
             }
           }
-          p += c < 2 ? c : 2u;
+          p += c < 3 ? c : 3u;
         }
         stg[p] = x;
       }
