@@ -994,11 +994,30 @@ __global__ void __launch_bounds__(BLOCK + 32) scatter_ws_kernel(Ws ws, int L) {
       // count (shared RED), scan, then place by atomic cursors -- no ranks
       // kept in registers, no per-key lookup of the tile digit start
       K x[KPT];
+      // A warp whose 32 keys share one digit (sorted or heavily skewed input)
+      // does one aggregated atomic instead of 32 same-address ones.
+      // The check costs a shuffle and a vote per key, so a warp only uses it
+      // when its first 32 keys already share a digit.
+      bool skew = false;
       if (fullt) {
 #pragma unroll
-        for (int j = 0; j < KPT; ++j) {
-          x[j] = kb[f.headk + j * BLOCK + tid];
-          atomicAdd(&cnt256[dfn(x[j])], 1u);
+        for (int j = 0; j < KPT; ++j) x[j] = kb[f.headk + j * BLOCK + tid];
+        const uint32_t e0 = dfn(x[0]);
+        skew = __all_sync(0xFFFFFFFFu, e0 == __shfl_sync(0xFFFFFFFFu, e0, 0));
+        if (skew) {
+#pragma unroll
+          for (int j = 0; j < KPT; ++j) {
+            const uint32_t d = dfn(x[j]);
+            const uint32_t d0 = __shfl_sync(0xFFFFFFFFu, d, 0);
+            if (__all_sync(0xFFFFFFFFu, d == d0)) {
+              if (lane == 0) atomicAdd(&cnt256[d0], 32u);
+            } else {
+              atomicAdd(&cnt256[d], 1u);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < KPT; ++j) atomicAdd(&cnt256[dfn(x[j])], 1u);
         }
       } else {
 #pragma unroll
@@ -1021,9 +1040,24 @@ __global__ void __launch_bounds__(BLOCK + 32) scatter_ws_kernel(Ws ws, int L) {
         gbase[tid] = uint32_t(f.start - uint64_t(f.tin) * TILE) + base - texcl;
       }
       named_sync<BLOCK>();
-      if (fullt) {
+      if (fullt && !skew) {
 #pragma unroll
         for (int j = 0; j < KPT; ++j) kb[atomicAdd(&tstart[dfn(x[j])], 1u)] = x[j];
+      } else if (fullt) {
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+          const uint32_t d = dfn(x[j]);
+          const uint32_t d0 = __shfl_sync(0xFFFFFFFFu, d, 0);
+          uint32_t pos;
+          if (__all_sync(0xFFFFFFFFu, d == d0)) {
+            uint32_t b0 = 0;
+            if (lane == 0) b0 = atomicAdd(&tstart[d0], 32u);
+            pos = __shfl_sync(0xFFFFFFFFu, b0, 0) + uint32_t(lane);
+          } else {
+            pos = atomicAdd(&tstart[d], 1u);
+          }
+          kb[pos] = x[j];
+        }
       } else {
 #pragma unroll
         for (int j = 0; j < KPT; ++j)
