@@ -394,14 +394,48 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
     const K spanmask = (spanv >= W ? ~K(0) : ((K(1) << spanv) - 1)) << lbv;
     const K dmask = K(0xFF) << lowbits;
     const K cbase = K(ws.bor[cur][b]) & ~spanmask & ~dmask;
+    // Dense children are the common case (every child of a uniform bucket):
+    // reserve their list slots with one atomic per parent, not one per child.
+    auto is_dense = [&](const Emit &e) {
+      return e.kind == 1 && !(e.count == 1 && cpar == 0) && dense && e.digit != 0xFFFFFFFFu &&
+             e.count > 1 && e.count <= big_max;
+    };
+    // Same for the next level's buckets and their tiles.
+    uint32_t mine = 0;   // small | big << 16
+    uint32_t mbk = 0;    // large children (next-level buckets)
+    uint32_t mtile = 0;  // their tiles
+    for (uint32_t i = tid; i < ne; i += 256) {
+      const Emit e = s_emit[i];
+      if (is_dense(e)) mine += (e.count > ws.dense_max) ? 0x10000u : 1u;
+      if (e.kind == 0) {
+        mbk += 1;
+        mtile += uint32_t((e.count + ws.tile - 1) / ws.tile);
+      }
+    }
+    // packed block scans: (small | big << 16) and (buckets | tiles << 9);
+    // per parent small <= 520, big <= 256, buckets <= 256, tiles < 2^23
+    const uint32_t mexcl = scan256_excl<256>(mine, s_scan);
+    const uint32_t bexcl = scan256_excl<256>(mbk | (mtile << 9), s_scan);
+    __shared__ uint32_t s_dbase[4];
+    if (tid == 255) {
+      const uint32_t tot = mexcl + mine;
+      const uint32_t btot = bexcl + (mbk | (mtile << 9));
+      s_dbase[0] = (tot & 0xFFFFu) ? atomicAdd(&ws.ctl->ndtasks, tot & 0xFFFFu) : 0u;
+      s_dbase[1] = (tot >> 16) ? atomicAdd(&ws.ctl->ndtasks_big, tot >> 16) : 0u;
+      s_dbase[2] = (btot & 0x1FFu) ? atomicAdd(&ws.ctl->nbuckets[L + 1], btot & 0x1FFu) : 0u;
+      s_dbase[3] = (btot >> 9) ? atomicAdd(&ws.ctl->ntiles[L + 1], btot >> 9) : 0u;
+    }
+    __syncthreads();
+    uint32_t ksmall = s_dbase[0] + (mexcl & 0xFFFFu), kbig = s_dbase[1] + (mexcl >> 16);
+    uint32_t kbk = s_dbase[2] + (bexcl & 0x1FFu), ktile = s_dbase[3] + (bexcl >> 9);
     for (uint32_t i = tid; i < ne; i += 256) {
       const Emit e = s_emit[i];
       if (e.kind == 1) {
         if (e.count == 1 && cpar == 0) continue;  // singleton already home: done
-        if (dense && e.digit != 0xFFFFFFFFu && e.count > 1 && e.count <= big_max) {
+        if (is_dense(e)) {
           // small dense tasks fill the list from the front, big ones from the back
           const bool big = e.count > ws.dense_max;
-          const uint32_t k = atomicAdd(big ? &ws.ctl->ndtasks_big : &ws.ctl->ndtasks, 1u);
+          const uint32_t k = big ? kbig++ : ksmall++;
           if (k < ws.maxtasks / 2) {
             const uint32_t slot = big ? ws.maxtasks - 1 - k : k;
             ws.dtasks[slot] = DTask{e.start, uint64_t(cbase | (K(e.digit) << lowbits)), e.count,
@@ -414,7 +448,11 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
           emit_tasks(ws, e.start, e.count, cpar);
         }
       } else {
-        push_bucket(ws, L, e.start, e.count, uint32_t(dig + 1), cpar);
+        const uint32_t nt = uint32_t((e.count + ws.tile - 1) / ws.tile);
+        const uint32_t slot = kbk++, t0 = ktile;
+        ktile += nt;
+        if (slot >= ws.maxb || t0 + nt > ws.maxtiles) atomicOr(&ws.ctl->error, 3u);
+        else ws.buckets[(L + 1) & 1][slot] = Bucket{e.start, e.count, t0, uint32_t(dig + 1), cpar, ACT_SCATTER, 0};
       }
     }
     __syncthreads();
