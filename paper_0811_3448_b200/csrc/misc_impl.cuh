@@ -277,7 +277,6 @@ __global__ void __launch_bounds__(SPLIT_BLOCK) split_scatter_kernel(
   const KeyGeom<K, KIND> g{shift0};
   __shared__ uint32_t whist_all[NW * 256];
   __shared__ uint32_t tstart[256];
-  __shared__ uint32_t misc[32];
   __shared__ K s_spl[16];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   if (tid < nsp) s_spl[tid] = spl[tid];

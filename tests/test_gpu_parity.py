@@ -155,7 +155,19 @@ DISTS = {
     "few_u64": lambda n: np.random.default_rng(2).integers(0, 5, n).astype(np.uint64) << np.uint64(40),
     "dup_heavy_u32": lambda n: np.random.default_rng(4).integers(0, 300, n).astype(np.uint32) * np.uint32(65537),
     "dense16_u32": lambda n: np.random.default_rng(5).integers(0, 1 << 16, n).astype(np.uint32),
+    # dense local-sort tasks with second/third/fourth+ copies (B2, B3, overflow list)
+    "dense_dups_u32": lambda n: _top_low(6, n, 1 << 10, 1 << 12),
+    "dense_dups_sparse_u32": lambda n: _top_low(7, n, 1 << 10, 1 << 13),
+    # ~16K-key tasks for the big dense variant, with a few repeats
+    "big_dense_u32": lambda n: _top_low(8, n, 1 << 8, 1 << 16),
 }
+
+
+def _top_low(seed, n, ntop, nlow):
+    """u32 keys: top 16 bits from `ntop` values, low 16 bits from [0, nlow)."""
+    r = np.random.default_rng(seed)
+    top = (r.integers(0, ntop, n).astype(np.uint32) * np.uint32(40503)) & np.uint32(0xFFFF)
+    return (top << np.uint32(16)) | r.integers(0, nlow, n).astype(np.uint32)
 
 
 @pytest.mark.parametrize("name", sorted(DISTS))
