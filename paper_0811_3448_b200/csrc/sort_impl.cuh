@@ -361,34 +361,52 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
     // (big ones only while dense enough that repeats stay rare: n <= 2^span / 3.5)
     const uint32_t big_max =
         dense ? max(ws.local_max, min(ws.dense_big_max, uint32_t((2ull << spanv) / 7))) : ws.local_max;
-    __syncthreads();
-    if (tid == 0) {
-      // greedy in digit order: large children go to the next level, mid-size
-      // ones become local tasks, small ones are grouped up to local_max
-      uint32_t ne = 0;
-      uint64_t gs = 0;
-      uint32_t gc = 0;
-      uint64_t pos = bk.start;
-      for (int d = 0; d < 256; ++d) {
-        const uint32_t cd = s_cnt[d];
-        if (cd == 0) continue;
-        if (cd >= ws.group_min) {
-          if (gc) s_emit[ne++] = Emit{gs, gc, 1, 0xFFFFFFFFu};
-          gc = 0;
-          s_emit[ne++] = Emit{pos, cd, cd > big_max ? 0u : 1u, uint32_t(d)};
-        } else {
-          if (gc + cd > ws.local_max) {
-            s_emit[ne++] = Emit{gs, gc, 1, 0xFFFFFFFFu};
-            gc = 0;
-          }
-          if (gc == 0) gs = pos;
-          gc += cd;
-        }
-        pos += cd;
+    // Greedy grouping in digit order, in parallel: large children (>= group_min)
+    // are emitted on their own; each run of small children between two large
+    // ones is packed greedily (groups <= local_max) by the run's first digit.
+    const uint32_t cd = c;
+    const bool isbig = cd >= ws.group_min, issmall = cd > 0 && !isbig;
+    __shared__ uint32_t s_bigm[8], s_smallm[8], s_excl[256];
+    {
+      const uint32_t bm = __ballot_sync(0xFFFFFFFFu, isbig), sm = __ballot_sync(0xFFFFFFFFu, issmall);
+      if ((tid & 31) == 0) {
+        s_bigm[tid >> 5] = bm;
+        s_smallm[tid >> 5] = sm;
       }
-      if (gc) s_emit[ne++] = Emit{gs, gc, 1, 0xFFFFFFFFu};
-      s_nemit = ne;
+      s_excl[tid] = excl;
     }
+    __syncthreads();
+    auto last_below = [&](const uint32_t *m, int d) -> int {  // highest set bit < d, or -1
+      for (int wd = d >> 5; wd >= 0; --wd) {
+        const uint32_t x = m[wd] & (wd == (d >> 5) ? ((1u << (d & 31)) - 1u) : 0xFFFFFFFFu);
+        if (x) return wd * 32 + 31 - __clz(x);
+      }
+      return -1;
+    };
+    const bool leader = issmall && last_below(s_smallm, tid) <= last_below(s_bigm, tid);
+    // run leaders walk their run twice: count the groups, then write them
+    auto walk = [&](uint32_t slot, bool write) -> uint32_t {
+      uint32_t k = 0, gc = 0, gs = 0;
+      for (int d = tid; d < 256; ++d) {
+        const uint32_t cdd = s_cnt[d];
+        if (cdd >= ws.group_min) break;
+        if (cdd == 0) continue;
+        if (gc + cdd > ws.local_max) {
+          if (write) s_emit[slot + k] = Emit{bk.start + gs, gc, 1, 0xFFFFFFFFu};
+          ++k;
+          gc = 0;
+        }
+        if (gc == 0) gs = s_excl[d];
+        gc += cdd;
+      }
+      if (write) s_emit[slot + k] = Emit{bk.start + gs, gc, 1, 0xFFFFFFFFu};
+      return k + 1;
+    };
+    const uint32_t myn = isbig ? 1u : (leader ? walk(0, false) : 0u);
+    const uint32_t eoff = scan256_excl<256>(myn, s_scan);
+    if (tid == 255) s_nemit = eoff + myn;
+    if (isbig) s_emit[eoff] = Emit{bk.start + excl, cd, cd > big_max ? 0u : 1u, uint32_t(tid)};
+    else if (leader) walk(eoff, true);
     __syncthreads();
     const uint32_t ne = s_nemit;
     const K spanmask = (spanv >= W ? ~K(0) : ((K(1) << spanv) - 1)) << lbv;
