@@ -37,6 +37,25 @@ static int fail(int code, const std::string &msg) {
       return fail(BS_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
   } while (0)
 
+// Launch with programmatic stream serialisation: the kernel may be scheduled
+// while its predecessor in the stream drains (every kernel of the sort starts
+// with pdl_wait()), hiding most of the launch gap between dependent kernels.
+template <typename... KArgs, typename... Args>
+static cudaError_t pdl_launch(void (*kern)(KArgs...), int grid, int block, size_t smem, cudaStream_t st,
+                              Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(unsigned(block));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 static int num_sms() {
   static int sms = 0;
   static std::once_flag once;
@@ -214,30 +233,31 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   {
     const uint32_t ntiles = uint32_t((n + geo.tile - 1) / geo.tile);
     const int g = int(min64((ntiles + 255) / 256 + 1, 4096));
-    init_kernel<K, KIND><<<g, 256, 0, st>>>(ws);
+    BS_CUDA(pdl_launch(init_kernel<K, KIND>, g, 256, 0, st, ws));
   }
   mark(st);
   if (n > geo.local_max) {
     const int nlev = geo.ndig + 1;
     for (int L = 0; L < nlev; ++L) {
-      hk<<<hk_grid, HI_BLOCK, 0, st>>>(ws, L);
+      BS_CUDA(pdl_launch(hk, hk_grid, HI_BLOCK, 0, st, ws, L));
       mark(st);
-      plan_kernel<K><<<num_sms() * 4, 256, 0, st>>>(ws, L);
+      BS_CUDA(pdl_launch(plan_kernel<K>, num_sms() * 4, 256, 0, st, ws, L));
       mark(st);
-      if constexpr (WSPEC) sw<<<sc_grid, SC_BLOCK + 32, SW::bytes, st>>>(ws, L);
-      else sc<<<sc_grid, SC_BLOCK, SS::bytes, st>>>(ws, L);
+      if constexpr (WSPEC) BS_CUDA(pdl_launch(sw, sc_grid, SC_BLOCK + 32, SW::bytes, st, ws, L));
+      else BS_CUDA(pdl_launch(sc, sc_grid, SC_BLOCK, SS::bytes, st, ws, L));
       if constexpr (VB == 0) {
         // big dense children of this level (their data is in place now)
-        if (ws.dense && ws.dense_big_max && L < nlev - 1) db<<<db_grid, DN_BLOCK + 32, DB::bytes, st>>>(ws, L);
+        if (ws.dense && ws.dense_big_max && L < nlev - 1)
+          BS_CUDA(pdl_launch(db, db_grid, DN_BLOCK + 32, DB::bytes, st, ws, L));
       }
-      expand_kernel<<<num_sms() * 4, 256, 0, st>>>(ws, L + 1);
+      BS_CUDA(pdl_launch(expand_kernel, num_sms() * 4, 256, 0, st, ws, L + 1));
       mark(st);
     }
   }
   if constexpr (VB == 0) {
-    if (ws.dense) dk<<<dk_grid, DN_BLOCK + 32, DS::bytes, st>>>(ws, 0);
+    if (ws.dense) BS_CUDA(pdl_launch(dk, dk_grid, DN_BLOCK + 32, DS::bytes, st, ws, 0));
   }
-  lc<<<lc_grid, LC_BLOCK, LS::bytes, st>>>(ws);
+  BS_CUDA(pdl_launch(lc, lc_grid, LC_BLOCK, LS::bytes, st, ws));
   mark(st);
   BS_CUDA(cudaGetLastError());
   return BS_OK;

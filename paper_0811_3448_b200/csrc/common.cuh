@@ -240,6 +240,12 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       : "memory");
 }
 
+// Programmatic dependent launch: a kernel launched with the programmatic
+// stream-serialisation attribute may start while the previous kernel in the
+// stream drains; it must wait here before touching anything that kernel
+// produces or reads.  A no-op for ordinary launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Bulk shared -> global store (async proxy), tracked by the issuing thread's
 // bulk async-groups.  Addresses 16-byte aligned, size a multiple of 16.
 __device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes) {

@@ -127,6 +127,7 @@ struct Ws {
 // ---------------------------------------------------------------------------
 template <typename K, int KIND>
 __global__ void init_kernel(Ws ws) {
+  pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
   const int tid = threadIdx.x;
   const uint64_t n = ws.n;
   const KeyGeom<K, KIND> g{ws.shift0};
@@ -184,6 +185,7 @@ __global__ void init_kernel(Ws ws) {
 // ---------------------------------------------------------------------------
 template <typename K, int KIND, int BLOCK, int KPT>
 __global__ void __launch_bounds__(BLOCK) hist_kernel(Ws ws, int L) {
+  pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
   constexpr int NCOPY = 4;
   __shared__ uint32_t h[NCOPY][256];
   __shared__ uint64_t s_or[BLOCK / 32], s_and[BLOCK / 32];
@@ -309,6 +311,7 @@ __device__ __forceinline__ void push_bucket(const Ws &ws, int L, uint64_t start,
 
 template <typename K>
 __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
+  pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
   constexpr int W = KeyTraits<K>::BITS;
   __shared__ uint32_t s_cnt[256];
   __shared__ uint32_t s_scan[16];
@@ -480,6 +483,7 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
 // expand: for every bucket of level L, clear its histogram row / masks and
 // map its tiles (tile -> bucket).  One warp per bucket.
 __global__ void __launch_bounds__(256) expand_kernel(Ws ws, int L) {
+  pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
   const int cur = L & 1;
   const uint32_t nb = min(ws.ctl->nbuckets[L], ws.maxb);
   const int lane = threadIdx.x & 31;
@@ -710,6 +714,7 @@ struct ScatterSmem {
 
 template <typename K, int VB, int KIND, int BLOCK, int KPT>
 __global__ void __launch_bounds__(BLOCK) scatter_kernel(Ws ws, int L) {
+  pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
   using S = ScatterSmem<K, VB, KIND, BLOCK, KPT>;
   using D = typename S::D;
   using V = typename S::V;
@@ -975,6 +980,7 @@ __device__ __forceinline__ uint32_t scan256_excl_nb(uint32_t v, uint32_t *scratc
 
 template <typename K, int KIND, int BLOCK, int KPT, int NBUF>
 __global__ void __launch_bounds__(BLOCK + 32) scatter_ws_kernel(Ws ws, int L) {
+  pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
   using S = ScatterWsSmem<K, KIND, BLOCK, KPT, NBUF>;
   constexpr int TILE = S::TILE;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -1211,6 +1217,7 @@ __device__ __forceinline__ void for_slots(int jn, int jfull, F &&f) {
 
 template <typename K, int KIND, int BLOCK, int KPT, int NSLOT, bool BIG>
 __global__ void __launch_bounds__(BLOCK + 32, BIG ? 1 : 2) dense_kernel(Ws ws, int L) {
+  pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
   using S = DenseSmem<K, BLOCK, KPT, NSLOT>;
   extern __shared__ __align__(128) unsigned char smem[];
   uint32_t *B1 = reinterpret_cast<uint32_t *>(smem + S::b1_off);
@@ -1548,6 +1555,7 @@ struct LocalSmem {
 
 template <typename K, int VB, int KIND, int BLOCK, int KPT>
 __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
+  pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
   using S = LocalSmem<K, VB, KIND, BLOCK, KPT>;
   using D = typename S::D;
   using V = typename S::V;
