@@ -13,6 +13,7 @@
 #include "metrics_impl.cuh"
 #include "misc_impl.cuh"
 #include "sort_impl.cuh"
+#include "dense_impl.cuh"
 
 namespace bs {
 
@@ -194,17 +195,17 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   constexpr bool WSPEC = VB == 0;  // keys-only: warp-specialised scatter
   auto sc = scatter_kernel<K, VB, KIND, SC_BLOCK, SKPT>;
   auto sw = scatter_ws_kernel<K, KIND, SC_BLOCK, SKPT, SC_NBUF>;
-  // dense local sort: 512 consumers x 11 keys (5632-key tasks), 2-slot ring;
-  // big variant (u32 only) 512 x 36 (18432-key tasks, e.g. 2^30-key inputs),
-  // single slot
-  constexpr int DN_BLOCK = 512, DN_KPT = 11, DN_SLOTS = 2;
-  constexpr int DB_KPT = sizeof(K) == 4 ? 36 : 12;
-  using DS = DenseSmem<K, DN_BLOCK, DN_KPT, DN_SLOTS>;
-  using DB = DenseSmem<K, DN_BLOCK, DB_KPT, 1>;
-  auto dk = dense_kernel<K, KIND, DN_BLOCK, DN_KPT, DN_SLOTS, false>;
-  auto db = dense_kernel<K, KIND, DN_BLOCK, DB_KPT, 1, true>;
-  ws.dense_max = DN_BLOCK * DN_KPT;
-  ws.dense_big_max = sizeof(K) == 4 ? DN_BLOCK * DB_KPT : 0;
+  // dense local sort (bitmap enumeration): 512 consumers, 5632-key tasks,
+  // 2-slot ring; big variant (u32 only) 18432-key tasks (e.g. 2^30-key
+  // inputs), single slot
+  constexpr int DN_BLOCK = 512, DN_CAP = 5632, DN_SLOTS = 2;
+  constexpr int DB_CAP = sizeof(K) == 4 ? 18432 : 6144;
+  using DS = DenseSmem<K, DN_BLOCK, DN_CAP, DN_SLOTS>;
+  using DB = DenseSmem<K, DN_BLOCK, DB_CAP, 1>;
+  auto dk = dense_kernel<K, KIND, DN_BLOCK, DN_CAP, DN_SLOTS, false>;
+  auto db = dense_kernel<K, KIND, DN_BLOCK, DB_CAP, 1, true>;
+  ws.dense_max = DN_CAP;
+  ws.dense_big_max = sizeof(K) == 4 ? DB_CAP : 0;
   auto lc = local_kernel<K, VB, KIND, LC_BLOCK, LC_KPT>;
   auto hk = hist_kernel<K, KIND, HI_BLOCK, HKPT>;
   static int sc_grid = 0, lc_grid = 0, hk_grid = 0, dk_grid = 0, db_grid = 0;

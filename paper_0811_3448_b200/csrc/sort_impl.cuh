@@ -1147,378 +1147,6 @@ __global__ void __launch_bounds__(BLOCK + 32) scatter_ws_kernel(Ws ws, int L) {
 }
 
 // ---------------------------------------------------------------------------
-// K4a: dense keys-only local sort (the common case after two 8-bit MSD levels
-// of full-width keys: each task's keys differ only inside a 16-bit span).
-// Counting sort through per-task bitmaps, warp-specialised like the scatter:
-// a producer warp streams tasks in by TMA into a two-slot ring while BLOCK
-// consumer threads sort the previous one.
-//   insert:  each key is loaded once into registers (the input slot is then
-//            released) and sets its bit in the presence bitmap B1 with one
-//            shared atomicOr.  A key that finds its bit set is a repeat:
-//            second copies set B2, later ones go to a small overflow list;
-//            every repeat adds one to its word's extra-copy count XC (the
-//            first B2 / overflow entry of a word also flags the word).
-//   scan:    per-word key counts popc(B1) + XC -> exclusive word prefix,
-//            written over XC (flags kept in the top bits);
-//   place:   pos = prefix + popc(B1 & below) [+ popc(B2 & below)] + copy
-//            index into the staging buffer (keys of words with overflow
-//            entries also count the listed smaller values); one thread then
-//            stores the task to HBM with a bulk async copy while the block
-//            moves on.
-// A task with more repeats than the overflow list holds is handed to the
-// general local sort (small variant) or to the next MSD level (big variant).
-// ---------------------------------------------------------------------------
-template <typename K, int BLOCK, int KPT, int NSLOT>
-struct DenseSmem {
-  static constexpr int CAP = BLOCK * KPT;
-  static constexpr int NW = 2048;      // 2^16 values / 32
-  static constexpr int DUPCAP = CAP > 8192 ? 1024 : 256;  // fourth+ copies
-  static constexpr size_t kbuf = (sizeof(K) * CAP + 32 + 15) & ~size_t(15);
-  static constexpr size_t dbuf_off = 0;
-  static constexpr size_t stg_off = dbuf_off + NSLOT * kbuf;  // staging (+16: alignment shift)
-  // structure-of-arrays bitmaps: random words spread over all 32 banks
-  static constexpr size_t b1_off = stg_off + kbuf + 16;
-  static constexpr size_t xc_off = b1_off + sizeof(uint32_t) * NW;  // extra copies, then prefix
-  static constexpr size_t b2_off = xc_off + sizeof(uint32_t) * NW;
-  static constexpr size_t b3_off = b2_off + sizeof(uint32_t) * NW;
-  static constexpr size_t cp_off = b3_off + sizeof(uint32_t) * NW;  // copy index of repeated keys
-  static constexpr size_t dup_off = (cp_off + sizeof(uint16_t) * CAP + 15) & ~size_t(15);
-  static constexpr size_t dmy_off = dup_off + sizeof(uint32_t) * DUPCAP;  // atomics of idle lanes
-  static constexpr size_t misc_off = dmy_off + sizeof(uint32_t) * 32;
-  static constexpr size_t bars_off = misc_off + sizeof(uint32_t) * 64;
-  static constexpr size_t info_off = bars_off + sizeof(uint64_t) * 2 * NSLOT;
-  static constexpr size_t bytes = info_off + sizeof(InFlight) * NSLOT;
-};
-
-// Calls f(j, full) for j < jn (block-uniform), where `full` is a
-// std::true_type when every thread's slot j holds a key (j < jfull) and a
-// std::false_type otherwise: groups of four up to C4 so independent
-// shared-memory round trips overlap, single steps after.
-template <int KPT, int C4, typename F>
-__device__ __forceinline__ void for_slots(int jn, int jfull, F &&f) {
-#pragma unroll
-  for (int j0 = 0; j0 < C4; j0 += 4) {
-    if (j0 + 4 <= jfull) {
-#pragma unroll
-      for (int jj = 0; jj < 4; ++jj)
-        if (j0 + jj < C4) f(j0 + jj, std::true_type{});
-    } else if (j0 < jn) {
-#pragma unroll
-      for (int jj = 0; jj < 4; ++jj)
-        if (j0 + jj < C4) f(j0 + jj, std::false_type{});
-    }
-  }
-#pragma unroll
-  for (int j = C4; j < KPT; ++j) {
-    if (j < jfull) f(j, std::true_type{});
-    else if (j < jn) f(j, std::false_type{});
-  }
-}
-
-template <typename K, int KIND, int BLOCK, int KPT, int NSLOT, bool BIG>
-__global__ void __launch_bounds__(BLOCK + 32, BIG ? 1 : 2) dense_kernel(Ws ws, int L) {
-  pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
-  using S = DenseSmem<K, BLOCK, KPT, NSLOT>;
-  extern __shared__ __align__(128) unsigned char smem[];
-  uint32_t *B1 = reinterpret_cast<uint32_t *>(smem + S::b1_off);
-  uint32_t *XC = reinterpret_cast<uint32_t *>(smem + S::xc_off);
-  uint32_t *B2 = reinterpret_cast<uint32_t *>(smem + S::b2_off);
-  uint32_t *B3 = reinterpret_cast<uint32_t *>(smem + S::b3_off);
-  uint16_t *cpv = reinterpret_cast<uint16_t *>(smem + S::cp_off);
-  uint32_t *dup = reinterpret_cast<uint32_t *>(smem + S::dup_off);
-  uint32_t *dmy = reinterpret_cast<uint32_t *>(smem + S::dmy_off);
-  uint32_t *misc = reinterpret_cast<uint32_t *>(smem + S::misc_off);
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + S::bars_off);
-  uint64_t *empty = full + NSLOT;
-  InFlight *info = reinterpret_cast<InFlight *>(smem + S::info_off);
-  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  // Small dense tasks: the whole list, after all levels.  Big ones: the tasks
-  // planned at level L, right after scatter(L), so one that overflows can
-  // still be pushed to level L+1 as an ordinary bucket.
-  const uint32_t k0 = BIG ? (L > 0 ? ws.ctl->dbig_end[L - 1] : 0u) : 0u;
-  const uint32_t nt = min(BIG ? ws.ctl->dbig_end[L] : ws.ctl->ndtasks, ws.maxtasks / 2) - min(k0, ws.maxtasks / 2);
-  if (blockIdx.x >= nt) return;
-  // big tasks are stored from the back of the list
-  auto task_at = [&](uint32_t k) -> const DTask & {
-    return ws.dtasks[BIG ? ws.maxtasks - 1 - (k0 + k) : k];
-  };
-  const KeyGeom<K, KIND> g{0};
-  if (tid == BLOCK) {
-    for (int i = 0; i < NSLOT; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  if (w == BLOCK / 32) {  // ---------------- producer warp ----------------
-    if (lane != 0) return;
-    uint32_t ti = blockIdx.x;
-    DTask nxt = task_at(ti);  // task records are fetched one task ahead
-    for (uint32_t i = 0;; ++i) {
-      const int s = int(i % NSLOT);
-      const DTask t = nxt;
-      const uint32_t tn = ti + gridDim.x;
-      if (tn < nt) nxt = task_at(tn);
-      if (i >= NSLOT) mbar_wait_sleep(&empty[s], ((i / NSLOT) - 1) & 1u);
-      InFlight f{};
-      f.idx = ti;
-      if (ti < nt) {
-        f.start = t.start;
-        f.cnt = t.count;
-        f.digit = t.meta;  // lb | span << 8 | parity << 16 | digit << 20
-        f.parity = (t.meta >> 16) & 1u;
-        const Span sk = span16(static_cast<const K *>(ws.keys[f.parity]) + f.start, f.cnt);
-        f.headk = sk.head;
-        info[s] = f;
-        fence_proxy_async_smem();
-        mbar_arrive_expect_tx(&full[s], sk.bytes);
-        bulk_g2s(smem + S::dbuf_off + s * S::kbuf, sk.base, sk.bytes, &full[s]);
-      } else {
-        info[s] = f;
-        mbar_arrive(&full[s]);
-        return;
-      }
-      ti = tn;
-    }
-  }
-
-  // ---------------- consumers ----------------
-  constexpr uint32_t F1 = 0x80000000u;  // word has overflow-list entries
-  constexpr uint32_t F2 = 0x40000000u;  // word has second copies (B2)
-  constexpr uint32_t F3 = 0x20000000u;  // word has third copies (B3)
-  constexpr uint32_t CM = 0x1FFFFFFFu;
-  constexpr int C4 = BIG ? KPT : (KPT < 8 ? KPT : 8);
-  constexpr int NWARP = BLOCK / 32;
-  static_assert(S::NW / 4 <= BLOCK, "one thread per four bitmap words");
-  using Mask = typename std::conditional<(KPT > 32), unsigned long long, uint32_t>::type;
-  // B2/B3 start clear; afterwards the owners of flagged words clear them
-  for (int q = tid; q < S::NW / 4; q += BLOCK) {
-    reinterpret_cast<uint4 *>(B2)[q] = make_uint4(0, 0, 0, 0);
-    reinterpret_cast<uint4 *>(B3)[q] = make_uint4(0, 0, 0, 0);
-  }
-  BS_PROBE_INIT();
-  for (uint32_t i = 0;; ++i) {
-    const int s = int(i % NSLOT);
-    BS_PROBE(8);
-    mbar_wait(&full[s], (i / NSLOT) & 1u);
-    BS_PROBE(9);
-    const InFlight f = info[s];
-    if (f.idx >= nt) break;
-    const K *kb = reinterpret_cast<const K *>(smem + S::dbuf_off + s * S::kbuf) + f.headk;
-    const int n = int(f.cnt);
-    const int jn = (n + BLOCK - 1) / BLOCK, jfull = n / BLOCK;
-    const int lb = int(f.digit & 0xFFu), span = int((f.digit >> 8) & 0xFFu);
-    const uint32_t vmask = (span >= 32) ? 0xFFFFFFFFu : ((1u << span) - 1u);
-    // bitmap words, rounded up to 4 per owner thread (vectorised zero/scan)
-    const int nw = span <= 7 ? 4 : (1 << (span - 5));
-    for (int q = tid; q < nw / 4; q += BLOCK) {
-      reinterpret_cast<uint4 *>(B1)[q] = make_uint4(0, 0, 0, 0);
-      reinterpret_cast<uint4 *>(XC)[q] = make_uint4(0, 0, 0, 0);
-    }
-    if (tid == 0) misc[32] = 0;  // overflow count
-    named_sync<BLOCK>();
-    BS_PROBE(10);
-    // ---- insert: keys into registers, one presence atomic each ----
-    K x[KPT];
-    Mask rep = 0;  // bit j: key j is not the first copy of its value
-    // all loads first, so the atomics below can be in flight together
-    for_slots<KPT, C4>(jn, jfull, [&](int j, auto) { x[j] = kb[j * BLOCK + tid]; });  // past n: stale slot words
-    for_slots<KPT, C4>(jn, jfull, [&](int j, auto full) {
-      const uint32_t idx = uint32_t(g.norm(x[j]) >> lb) & vmask;
-      const uint32_t bit = 1u << (idx & 31u);
-      if (decltype(full)::value) {
-        if (atomicOr(&B1[idx >> 5], bit) & bit) rep |= Mask(1) << j;
-      } else {
-        const bool v = j * BLOCK + tid < n;
-        uint32_t *wd = v ? &B1[idx >> 5] : &dmy[lane];
-        if ((atomicOr(wd, bit) & bit) && v) rep |= Mask(1) << j;
-      }
-    });
-    // rare: second copies -> B2, third -> B3, later ones -> overflow list
-    // (keys re-read from the slot, which is still held)
-    Mask rep3 = 0;  // bit j: key j is a third or later copy
-    for (Mask r = rep; r; r &= r - Mask(1)) {
-      const int j = (KPT > 32) ? (__ffsll(static_cast<long long>(r)) - 1) : (__ffs(static_cast<int>(r)) - 1);
-      const int e = j * BLOCK + tid;
-      const uint32_t idx = uint32_t(g.norm(kb[e]) >> lb) & vmask;
-      const uint32_t q = idx >> 5, bit = 1u << (idx & 31u);
-      const uint32_t o2 = atomicOr(&B2[q], bit);
-      uint32_t c = 1;
-      if (!(o2 & bit)) {
-        atomicAdd(&XC[q], o2 ? 1u : (1u | F2));
-      } else {
-        const uint32_t o3 = atomicOr(&B3[q], bit);
-        c = 2;
-        if (!(o3 & bit)) {
-          atomicAdd(&XC[q], o3 ? 1u : (1u | F3));
-        } else {
-          const uint32_t sl = atomicAdd(&misc[32], 1u);
-          atomicAdd(&XC[q], 1u);
-          atomicOr(&XC[q], F1);
-          if (sl < S::DUPCAP) dup[sl] = idx;
-          c = 3 + min(sl, uint32_t(S::DUPCAP));
-        }
-        rep3 |= Mask(1) << j;
-      }
-      cpv[e] = uint16_t(c);
-    }
-    named_sync<BLOCK>();
-    // every key is in registers: the input slot can be refilled
-    if (tid == 0) mbar_arrive(&empty[s]);
-    BS_PROBE(11);
-    const uint32_t ndup = misc[32];
-    if (ndup > S::DUPCAP) {
-      // too many repeats: hand the task to the general local sort (small) or
-      // to the next MSD level as an ordinary bucket (big)
-      if (tid == 0) {
-        if (BIG) push_bucket(ws, L, f.start, f.cnt, (f.digit >> 20) & 0xFu, f.parity & 1u);
-        else emit_tasks(ws, f.start, f.cnt, f.parity & 1u);
-      }
-      named_sync<BLOCK>();
-      for (int q = tid; q < S::NW / 4; q += BLOCK) {
-        reinterpret_cast<uint4 *>(B2)[q] = make_uint4(0, 0, 0, 0);
-        reinterpret_cast<uint4 *>(B3)[q] = make_uint4(0, 0, 0, 0);
-      }
-      named_sync<BLOCK>();
-      continue;
-    }
-    // ---- scan: word counts -> exclusive prefix | flags, over XC ----
-    // thread t owns words 4t..4t+3: one uint4 of B1 and of XC, conflict-free
-    const bool own = 4 * tid < nw;
-    uint4 xc = make_uint4(0, 0, 0, 0);
-    {
-      uint4 b1 = make_uint4(0, 0, 0, 0);
-      if (own) {
-        b1 = reinterpret_cast<const uint4 *>(B1)[tid];
-        xc = reinterpret_cast<const uint4 *>(XC)[tid];
-      }
-      const uint32_t c0 = __popc(b1.x) + (xc.x & CM), c1 = __popc(b1.y) + (xc.y & CM);
-      const uint32_t c2 = __popc(b1.z) + (xc.z & CM), c3 = __popc(b1.w) + (xc.w & CM);
-      const uint32_t c = c0 + c1 + c2 + c3;
-      uint32_t incl = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      if (lane == 31) misc[w] = incl;
-      // the previous task's staging store must have left shared memory
-      // before this task's placement overwrites it
-      if (tid == 0) bulk_wait_read0();
-      named_sync<BLOCK>();
-      // warp bases: exclusive scan of the warp totals, one per lane
-      const uint32_t wt = lane < NWARP ? misc[lane] : 0u;
-      uint32_t wi = wt;
-#pragma unroll
-      for (int o = 1; o < NWARP; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, wi, o);
-        if (lane >= o) wi += y;
-      }
-      const uint32_t run = __shfl_sync(0xFFFFFFFFu, wi - wt, w) + incl - c;
-      if (own)
-        reinterpret_cast<uint4 *>(XC)[tid] =
-            make_uint4(run | (xc.x & ~CM), (run + c0) | (xc.y & ~CM), (run + c0 + c1) | (xc.z & ~CM),
-                       (run + c0 + c1 + c2) | (xc.w & ~CM));
-    }
-    named_sync<BLOCK>();
-    BS_PROBE(12);
-    // ---- place into the staging buffer (shifted to the output's 16-byte phase) ----
-    K *dst = static_cast<K *>(ws.keys[0]) + f.start;
-    const uint32_t mis = uint32_t(reinterpret_cast<uintptr_t>(dst) & 15u);
-    K *stg = reinterpret_cast<K *>(smem + S::stg_off + mis);
-    // Words with overflow entries: the listed copies of smaller values in the
-    // same word, and an overflow key's rank among its value's listed copies.
-    auto overflow_adj = [&](int j, uint32_t idx) -> uint32_t {
-      const uint32_t q = idx >> 5;
-      const uint32_t c = ((rep >> j) & Mask(1)) ? uint32_t(cpv[j * BLOCK + tid]) : 0u;
-      // an overflow key's copy index is 3 + rank; rep + rep3 counted 2
-      uint32_t a = c >= 3 ? 1u : 0u;
-      for (uint32_t t = 0; t < ndup; ++t) {
-        const uint32_t o = dup[t];
-        a += ((o >> 5) == q && o < idx) ? 1u : 0u;
-        a += (c >= 3 && o == idx && t < c - 3u) ? 1u : 0u;
-      }
-      return a;
-    };
-    // per group of four: positions first (loads only), then the stores, so
-    // no load waits behind a store it might alias
-    auto place4 = [&](int j0, auto full) {
-      constexpr bool FULL = decltype(full)::value;
-      uint32_t pp[4], fany = 0;
-#pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        const int j = j0 + jj;
-        if (j < KPT) {
-          const bool v = FULL || j * BLOCK + tid < n;
-          const uint32_t idx = uint32_t(g.norm(x[j]) >> lb) & vmask;
-          const uint32_t q = idx >> 5;
-          const uint32_t below = (1u << (idx & 31u)) - 1u;
-          const uint32_t b1 = v ? B1[q] : 0u;
-          const uint32_t xp = v ? XC[q] : 0u;
-          uint32_t p = (xp & CM) + __popc(b1 & below) + uint32_t((rep >> j) & Mask(1)) +
-                       uint32_t((rep3 >> j) & Mask(1));
-          if (xp & F2) p += __popc(B2[q] & below);
-          if (xp & F3) p += __popc(B3[q] & below);
-          fany |= xp;
-          pp[jj] = p;
-        }
-      }
-      if (fany & F1) {  // rare: fourth+ copies in play
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-          const int j = j0 + jj;
-          if (j < KPT && (FULL || j * BLOCK + tid < n)) {
-            const uint32_t idx = uint32_t(g.norm(x[j]) >> lb) & vmask;
-            if (XC[idx >> 5] & F1) pp[jj] += overflow_adj(j, idx);
-          }
-        }
-      }
-#pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
-        const int j = j0 + jj;
-        if (j < KPT && (FULL || j * BLOCK + tid < n)) stg[pp[jj]] = x[j];
-      }
-    };
-#pragma unroll
-    for (int j0 = 0; j0 < KPT; j0 += 4) {
-      if (j0 + 4 <= jfull) place4(j0, std::true_type{});
-      else if (j0 < jn) place4(j0, std::false_type{});
-    }
-    fence_proxy_async_smem();  // staging writes -> visible to the bulk copy
-    named_sync<BLOCK>();
-    BS_PROBE(13);
-    // ---- store: 16-byte-aligned middle by one bulk copy, ragged ends by threads ----
-    {
-      constexpr int EPG = 16 / int(sizeof(K));  // elements per 16-byte granule
-      const int h = min(n, mis ? int((16u - mis) / sizeof(K)) : 0);
-      const int m = ((n - h) / EPG) * EPG;
-      if (tid == 0 && m > 0) {
-        bulk_s2g(dst + h, stg + h, uint32_t(m) * uint32_t(sizeof(K)));
-        bulk_commit();
-      }
-      if (tid < h) dst[tid] = stg[tid];
-      if (h + m + tid < n) dst[h + m + tid] = stg[h + m + tid];
-    }
-    // owners clear the B2/B3 words of their flagged words
-    if (own && ((xc.x | xc.y | xc.z | xc.w) & (F2 | F3))) {
-      if (xc.x & F2) B2[4 * tid + 0] = 0;
-      if (xc.y & F2) B2[4 * tid + 1] = 0;
-      if (xc.z & F2) B2[4 * tid + 2] = 0;
-      if (xc.w & F2) B2[4 * tid + 3] = 0;
-      if (xc.x & F3) B3[4 * tid + 0] = 0;
-      if (xc.y & F3) B3[4 * tid + 1] = 0;
-      if (xc.z & F3) B3[4 * tid + 2] = 0;
-      if (xc.w & F3) B3[4 * tid + 3] = 0;
-    }
-    BS_PROBE(14);
-  }
-  if (tid == 0) bulk_wait0();
-  BS_PROBE_FLUSH();
-}
-
-// ---------------------------------------------------------------------------
 // K4: local sort of one task (<= BLOCK*KPT elements) per CTA iteration; the
 // next task streams in by TMA bulk copy while the current one is sorted.
 //  * Dense keys-only tasks (full-width words, all varying bits inside a
