@@ -113,7 +113,7 @@ static Geometry geometry(uint64_t n, int kb, int vb, int width_eff) {
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t ctl, buckets[2], bhist[2], bor[2], band[2], tile_bucket[2], status, tasks, dtasks, keys, vals, total;
+  size_t ctl, buckets[2], bhist[2], bor[2], band[2], tile_bucket[2], status, hist16, tasks, dtasks, keys, vals, total;
 };
 
 static Layout layout(const Geometry &g) {
@@ -133,6 +133,7 @@ static Layout layout(const Geometry &g) {
     l.tile_bucket[p] = take(sizeof(uint32_t) * g.maxtiles);
   }
   l.status = take(sizeof(uint32_t) * 256 * size_t(g.maxtiles));
+  l.hist16 = take(sizeof(uint32_t) * 65536);
   l.tasks = take(sizeof(Task) * g.maxtasks);
   l.dtasks = take(g.vb == 0 ? sizeof(DTask) * g.maxtasks : 0);
   l.keys = take(size_t(g.kb) * g.n);
@@ -168,6 +169,7 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
     ws.tile_bucket[p] = reinterpret_cast<uint32_t *>(base + lay.tile_bucket[p]);
   }
   ws.status = reinterpret_cast<uint32_t *>(base + lay.status);
+  ws.hist16 = reinterpret_cast<uint32_t *>(base + lay.hist16);
   ws.tasks = reinterpret_cast<Task *>(base + lay.tasks);
   ws.dtasks = reinterpret_cast<DTask *>(base + lay.dtasks);
   ws.keys[0] = keys;
@@ -183,6 +185,7 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   ws.group_min = geo.group_min;
   ws.ndig = geo.ndig;
   ws.shift0 = int(sizeof(K) * 8) - width_eff;
+  ws.kbits = int(sizeof(K) * 8);
   ws.stable = VB != 0;
   ws.dense = (VB == 0 && width_eff == int(sizeof(K) * 8)) ? 1 : 0;
 
@@ -208,6 +211,9 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   ws.dense_big_max = sizeof(K) == 4 ? DB_CAP : 0;
   auto lc = local_kernel<K, VB, KIND, LC_BLOCK, LC_KPT>;
   auto hk = hist_kernel<K, KIND, HI_BLOCK, HKPT>;
+  constexpr int H16_BLOCK = 1024;
+  constexpr size_t H16_SMEM = 32768 * sizeof(uint32_t);
+  auto h16 = hist16_kernel<K, KIND, H16_BLOCK>;
   static int sc_grid = 0, lc_grid = 0, hk_grid = 0, dk_grid = 0, db_grid = 0;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -226,6 +232,8 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
                     : num_sms() * max_active(sc, SC_BLOCK, SS::bytes);
     lc_grid = num_sms() * max_active(lc, LC_BLOCK, LS::bytes);
     hk_grid = num_sms() * max_active(hk, HI_BLOCK, 0);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(h16, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H16_SMEM));
   });
   if (attr_err != cudaSuccess) return fail(BS_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
 
@@ -240,7 +248,8 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   if (n > geo.local_max) {
     const int nlev = geo.ndig + 1;
     for (int L = 0; L < nlev; ++L) {
-      BS_CUDA(pdl_launch(hk, hk_grid, HI_BLOCK, 0, st, ws, L));
+      if (L == 0) BS_CUDA(pdl_launch(h16, num_sms(), H16_BLOCK, H16_SMEM, st, ws));
+      else BS_CUDA(pdl_launch(hk, hk_grid, HI_BLOCK, 0, st, ws, L));
       mark(st);
       BS_CUDA(pdl_launch(plan_kernel<K>, num_sms() * 4, 256, 0, st, ws, L));
       mark(st);

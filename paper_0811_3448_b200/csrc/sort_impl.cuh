@@ -64,8 +64,9 @@ struct Bucket {
   uint32_t digit;
   uint32_t parity;  // 0: live data in the caller's buffer, 1: in the workspace copy
   uint32_t action;
-  uint32_t pad;
+  uint32_t flags;  // BK_HKNOWN | parent digit << 8: histogram/masks filled by expand from hist16
 };
+constexpr uint32_t BK_HKNOWN = 1u;
 
 struct Task {
   uint64_t start;
@@ -91,6 +92,7 @@ struct Ctl {
   uint32_t error;        // bit 0: bucket overflow, 1: tile overflow, 2: task overflow
   uint32_t ndtasks_big;  // big dense tasks (back of dtasks)
   uint32_t dbig_end[MAXLEV + 1];  // ndtasks_big after plan(L) (snapshot by scatter(L))
+  uint32_t h16_bad;  // hist16 unusable (the root's digit is the last one)
 };
 
 // Workspace view (all device pointers), built on the host.
@@ -102,6 +104,7 @@ struct Ws {
   uint64_t *band[2];
   uint32_t *tile_bucket[2];
   uint32_t *status;  // [maxtiles][256]
+  uint32_t *hist16;  // [65536]: root histogram of the digit pair (dig, dig+1)
   Task *tasks;
   DTask *dtasks;
   int dense;           // keys-only full-width: dense tasks go to dense_kernel
@@ -116,6 +119,7 @@ struct Ws {
   uint32_t group_min;  // children smaller than this are grouped
   int ndig;            // number of 8-bit digits of the effective key
   int shift0;          // W - width_eff
+  int kbits;           // W
   int stable;          // key-value sort: tiles use the look-back scan
 };
 
@@ -142,6 +146,8 @@ __global__ void init_kernel(Ws ws) {
   for (uint32_t t = blockIdx.x * blockDim.x + tid; t < ntiles; t += gridDim.x * blockDim.x)
     ws.tile_bucket[0][t] = 0;
   for (int d = tid; d < 256; d += blockDim.x) ws.bhist[0][d] = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + tid; i < 65536u / 4; i += gridDim.x * blockDim.x)
+    reinterpret_cast<uint4 *>(ws.hist16)[i] = make_uint4(0, 0, 0, 0);
   if (blockIdx.x != 0) return;
   __shared__ uint64_t s_or[32], s_and[32];
   // 4096-element strided sample of the encoded normalised key
@@ -202,6 +208,7 @@ __global__ void __launch_bounds__(BLOCK) hist_kernel(Ws ws, int L) {
   K o = 0, a = ~K(0);
   uint32_t curb = 0xFFFFFFFFu;
   int dig = 0;
+  bool known = false;  // bucket's histogram and masks come from hist16
   __syncthreads();
   auto flush = [&](uint32_t b) {
     __syncthreads();
@@ -237,13 +244,15 @@ __global__ void __launch_bounds__(BLOCK) hist_kernel(Ws ws, int L) {
     const uint32_t b = ws.tile_bucket[cur][t];
     const Bucket bk = ws.buckets[cur][b];
     if (b != curb) {
-      if (curb != 0xFFFFFFFFu) flush(curb);
+      if (curb != 0xFFFFFFFFu && !known) flush(curb);
       curb = b;
       dig = int(bk.digit);
+      known = (bk.flags & BK_HKNOWN) != 0u;
     }
     // clear this tile's look-back row (256 x u32 = 64 x uint4)
     if (ws.stable && tid < 64)
       reinterpret_cast<uint4 *>(ws.status + size_t(t) * 256)[tid] = make_uint4(0, 0, 0, 0);
+    if (known) continue;
     const uint64_t off = uint64_t(t - bk.tile0) * ws.tile;
     const uint32_t cnt = uint32_t(min64(ws.tile, bk.count - off));
     const K *src = static_cast<const K *>(ws.keys[bk.parity]) + bk.start + off;
@@ -265,7 +274,121 @@ __global__ void __launch_bounds__(BLOCK) hist_kernel(Ws ws, int L) {
       }
     }
   }
-  flush(curb);
+  if (!known) flush(curb);
+}
+
+// ---------------------------------------------------------------------------
+// K1 at level 0: histogram of the digit PAIR (dig, dig+1) of the root bucket,
+// so the root's 256 children need no histogram pass of their own (plan(0)
+// marks them BK_HKNOWN; expand(1) copies their rows).  One CTA per SM keeps
+// 65536 16-bit bins in 128 KB of shared memory, two per word, each a 15-bit
+// count under a guard bit: the increment that sets a guard bit (old count
+// 0x7FFF) clears it again and moves 32768 to the global counts, so no carry
+// ever crosses into the neighbouring bin and the counts are exact for any
+// input.  Also yields the root's 256-bin histogram (row sums) and OR/AND
+// masks.
+// ---------------------------------------------------------------------------
+template <typename K, int KIND, int BLOCK>
+__global__ void __launch_bounds__(BLOCK, 1) hist16_kernel(Ws ws) {
+  pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
+  constexpr int W = KeyTraits<K>::BITS;
+  constexpr int EPG = 16 / int(sizeof(K));  // keys per 16-byte granule
+  constexpr int UNR = 4;                    // granules in flight per thread
+  extern __shared__ __align__(16) uint32_t hw[];  // 32768 words = 65536 u16 bins
+  __shared__ uint64_t s_or[BLOCK / 32], s_and[BLOCK / 32];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (ws.ctl->nbuckets[0] == 0) return;
+  const Bucket bk = ws.buckets[0][0];
+  const int dig = int(bk.digit);
+  const bool two = dig + 1 < ws.ndig;
+  const int sh8 = W - 8 - 8 * dig;
+  const int shA = two ? sh8 - 8 : sh8;
+  const uint32_t msk = two ? 0xFFFFu : 0xFFu, post = two ? 0u : 8u;
+  for (int i = tid; i < 32768 / 4; i += BLOCK) reinterpret_cast<uint4 *>(hw)[i] = make_uint4(0, 0, 0, 0);
+  if (!two && blockIdx.x == 0 && tid == 0) ws.ctl->h16_bad = 1u;
+  if (ws.stable) {  // clear the level-0 tiles' look-back rows (hist_kernel's job at other levels)
+    const uint32_t nq = ws.ctl->ntiles[0] * 64u;
+    for (uint32_t i = blockIdx.x * BLOCK + tid; i < nq; i += gridDim.x * BLOCK)
+      reinterpret_cast<uint4 *>(ws.status)[i] = make_uint4(0, 0, 0, 0);
+  }
+  __syncthreads();
+  const KeyGeom<K, KIND> g{ws.shift0};
+  const K *src = static_cast<const K *>(ws.keys[bk.parity]) + bk.start;
+  const uint64_t n = bk.count;
+  const uint32_t head = uint32_t((reinterpret_cast<uintptr_t>(src) & 15u) / sizeof(K));
+  const uint4 *gsrc = reinterpret_cast<const uint4 *>(src - head);
+  const uint64_t ng = (uint64_t(head) + n + EPG - 1) / EPG;
+  const uint64_t g0 = ng * blockIdx.x / gridDim.x, g1 = ng * (blockIdx.x + 1) / gridDim.x;
+  K o = 0, a = ~K(0);
+  auto count = [&](K x) {
+    const K nk = g.norm(x);
+    o |= nk;
+    a &= nk;
+    const uint32_t p = ((uint32_t(nk >> shA) & msk) << post);
+    const uint32_t sh = (p & 1u) << 4;
+    const uint32_t old = atomicAdd(&hw[p >> 1], 1u << sh);
+    if (((old >> sh) & 0xFFFFu) == 0x7FFFu) {  // guard bit just set: spill 32768
+      atomicSub(&hw[p >> 1], 0x8000u << sh);
+      atomicAdd(&ws.hist16[p], 32768u);
+      atomicAdd(&ws.bhist[0][p >> 8], 32768u);
+    }
+  };
+  auto granule = [&](uint64_t gi, const uint4 &v) {
+    K kk[EPG];
+    if constexpr (sizeof(K) == 4) {
+      kk[0] = K(v.x), kk[1] = K(v.y), kk[2 % EPG] = K(v.z), kk[3 % EPG] = K(v.w);
+    } else {
+      kk[0] = K((uint64_t(v.y) << 32) | v.x);
+      kk[1 % EPG] = K((uint64_t(v.w) << 32) | v.z);
+    }
+    const int64_t e0 = int64_t(gi * EPG) - int64_t(head);
+    if (e0 >= 0 && e0 + EPG <= int64_t(n)) {
+#pragma unroll
+      for (int j = 0; j < EPG; ++j) count(kk[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < EPG; ++j)
+        if (e0 + j >= 0 && e0 + j < int64_t(n)) count(kk[j]);
+    }
+  };
+  uint64_t gi = g0 + tid;
+  for (; gi + uint64_t(UNR - 1) * BLOCK < g1; gi += uint64_t(UNR) * BLOCK) {
+    uint4 v[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) v[u] = __ldcs(gsrc + gi + uint64_t(u) * BLOCK);
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) granule(gi + uint64_t(u) * BLOCK, v[u]);
+  }
+  for (; gi < g1; gi += BLOCK) granule(gi, __ldcs(gsrc + gi));
+  __syncthreads();
+  // flush: nonzero pair bins to hist16, row sums to the root's histogram
+  for (int i = tid; i < 32768; i += BLOCK) {
+    const uint32_t v = hw[i], lo = v & 0xFFFFu, hi = v >> 16;
+    if (two) {
+      if (lo) atomicAdd(&ws.hist16[2 * i], lo);
+      if (hi) atomicAdd(&ws.hist16[2 * i + 1], hi);
+    }
+    uint32_t sum = lo + hi;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, off);
+    if (lane == 0 && sum) atomicAdd(&ws.bhist[0][i >> 7], sum);  // 128 words per digit
+  }
+  const K oo = warp_or(o), aa = warp_and(a);
+  if (lane == 0) {
+    s_or[w] = oo;
+    s_and[w] = aa;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    K x = 0, y = ~K(0);
+    for (int i = 0; i < BLOCK / 32; ++i) {
+      x |= K(s_or[i]);
+      y &= K(s_and[i]);
+    }
+    atomicOr(reinterpret_cast<unsigned long long *>(&ws.bor[0][0]), (unsigned long long)x);
+    atomicAnd(reinterpret_cast<unsigned long long *>(&ws.band[0][0]),
+              (unsigned long long)(uint64_t(y) | (sizeof(K) == 4 ? 0xFFFFFFFF00000000ull : 0ull)));
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -342,6 +465,20 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
       }
       continue;
     }
+    if (bk.flags & BK_HKNOWN) {
+      // histogram from hist16, masks conservative (the root's): one occupied
+      // digit means the digit is constant here -- requeue on the next digit,
+      // which gets a real histogram pass
+      if (__syncthreads_count(c != 0u) == 1) {
+        if (tid == 0) {
+          ws.buckets[cur][b].action = ACT_SKIP;
+          if (bk.count <= ws.local_max) emit_tasks(ws, bk.start, bk.count, bk.parity);
+          else if (dig + 1 < ws.ndig) push_bucket(ws, L, bk.start, bk.count, uint32_t(dig + 1), bk.parity);
+          else if (bk.parity) emit_tasks(ws, bk.start, bk.count, 1);  // every digit constant: all equal
+        }
+        continue;
+      }
+    }
     // scatter this bucket on digit `dig`
     const uint32_t excl = scan256_excl<256>(c, s_scan);
     hist[tid] = excl;  // digit base within the bucket
@@ -349,6 +486,8 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
     if (tid == 0) ws.buckets[cur][b].action = ACT_SCATTER;
     const uint32_t cpar = bk.parity ^ 1u;
     const int lowbits = W - 8 - 8 * dig;
+    // the root's children take their histograms from hist16 (no hist pass at level 1)
+    const bool h16 = L == 0 && ws.ctl->h16_bad == 0u;
     const K lower = lowbits > 0 ? (var & ((K(1) << lowbits) - 1)) : K(0);
     if (lower == 0) {  // every child is all-equal: only a copy home may remain
       if (tid == 0 && cpar) emit_tasks(ws, bk.start, bk.count, 1);
@@ -473,7 +612,8 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
         const uint32_t slot = kbk++, t0 = ktile;
         ktile += nt;
         if (slot >= ws.maxb || t0 + nt > ws.maxtiles) atomicOr(&ws.ctl->error, 3u);
-        else ws.buckets[(L + 1) & 1][slot] = Bucket{e.start, e.count, t0, uint32_t(dig + 1), cpar, ACT_SCATTER, 0};
+        else ws.buckets[(L + 1) & 1][slot] =
+                 Bucket{e.start, e.count, t0, uint32_t(dig + 1), cpar, ACT_SCATTER, h16 ? (BK_HKNOWN | (e.digit << 8)) : 0u};
       }
     }
     __syncthreads();
@@ -492,10 +632,25 @@ __global__ void __launch_bounds__(256) expand_kernel(Ws ws, int L) {
   for (uint32_t b = gw; b < nb; b += nw) {
     const Bucket bk = ws.buckets[cur][b];
     uint4 *row = reinterpret_cast<uint4 *>(ws.bhist[cur] + size_t(b) * 256);
-    for (int i = lane; i < 64; i += 32) row[i] = make_uint4(0, 0, 0, 0);
-    if (lane == 0) {
-      ws.bor[cur][b] = 0;
-      ws.band[cur][b] = ~uint64_t(0);
+    if (bk.flags & BK_HKNOWN) {
+      // a child of the root: its digit histogram is row d0 of hist16; its
+      // masks are the root's with the parent digit fixed to d0 (a superset
+      // of the varying bits, which is all plan needs)
+      const uint32_t d0 = bk.flags >> 8;
+      const uint4 *src = reinterpret_cast<const uint4 *>(ws.hist16 + size_t(d0) * 256);
+      for (int i = lane; i < 64; i += 32) row[i] = src[i];
+      if (lane == 0) {
+        const int pos0 = ws.kbits - 8 - 8 * (int(bk.digit) - 1);
+        const uint64_t dm = 0xFFull << pos0, dv = uint64_t(d0) << pos0;
+        ws.bor[cur][b] = (ws.bor[0][0] & ~dm) | dv;
+        ws.band[cur][b] = (ws.band[0][0] & ~dm) | dv;
+      }
+    } else {
+      for (int i = lane; i < 64; i += 32) row[i] = make_uint4(0, 0, 0, 0);
+      if (lane == 0) {
+        ws.bor[cur][b] = 0;
+        ws.band[cur][b] = ~uint64_t(0);
+      }
     }
     const uint32_t nt = uint32_t((bk.count + ws.tile - 1) / ws.tile);
     for (uint32_t i = lane; i < nt; i += 32) ws.tile_bucket[cur][bk.tile0 + i] = b;

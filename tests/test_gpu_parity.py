@@ -366,3 +366,43 @@ def test_full_size_configs_match_reference(cuda, golden, name):
     assert sha(x) == g["input_sha"]
     out, _ = _sort_dev(x)
     assert sha(out) == g["output_sha"]
+
+
+# --------------------------------------------------------------------------
+# level-0 digit-pair histogram (hist16): bins past 32767 spill to the global
+# counts; constant second digits requeue with a real histogram pass
+# --------------------------------------------------------------------------
+
+def _heavy_prefix(n, seed):
+    """u32 keys, 7/8 of them under one 16-bit prefix (every CTA's bin spills)."""
+    r = np.random.default_rng(seed)
+    x = r.integers(0, 2 ** 32, n, dtype=np.uint64).astype(np.uint32)
+    heavy = r.random(n) < 0.875
+    x[heavy] = np.uint32(0xBEEF0000) | (x[heavy] & np.uint32(0xFFFF))
+    return x
+
+
+@pytest.mark.parametrize("kv", [False, True])
+def test_hist16_spills_exact(cuda, kv):
+    x = _heavy_prefix(1 << 24, 21)
+    if kv:
+        p = np.arange(x.size, dtype=np.uint32)
+        kk, pp = x.copy(), p.copy()
+        bs.sort(kk, UnsignedCodec(32), values=pp, with_metrics=False)
+        order = np.argsort(x, kind="stable")
+        assert np.array_equal(kk, x[order]) and np.array_equal(pp, p[order])
+    else:
+        got = x.copy()
+        bs.sort(got, UnsignedCodec(32), with_metrics=False)
+        assert np.array_equal(got, np.sort(x))
+
+
+def test_hist16_constant_second_digit(cuda):
+    # every root child has a constant second digit (one occupied hist16 bin per row)
+    r = np.random.default_rng(22)
+    top = r.integers(0, 256, 1 << 23).astype(np.uint32)
+    x = (top << np.uint32(24)) | ((top * np.uint32(37)) & np.uint32(0xFF)) << np.uint32(16) | \
+        r.integers(0, 1 << 16, top.size).astype(np.uint32)
+    got = x.copy()
+    bs.sort(got, UnsignedCodec(32), with_metrics=False)
+    assert np.array_equal(got, np.sort(x))
