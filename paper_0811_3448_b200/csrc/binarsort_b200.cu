@@ -113,7 +113,7 @@ static Geometry geometry(uint64_t n, int kb, int vb, int width_eff) {
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t ctl, buckets[2], bhist[2], bor[2], band[2], tile_bucket[2], status, hist16, tasks, dtasks, keys, vals, total;
+  size_t ctl, buckets[2], bhist[2], bor[2], band[2], tile_bucket[2], status, hist16, h16part, tasks, dtasks, keys, vals, total;
 };
 
 static Layout layout(const Geometry &g) {
@@ -134,6 +134,7 @@ static Layout layout(const Geometry &g) {
   }
   l.status = take(sizeof(uint32_t) * 256 * size_t(g.maxtiles));
   l.hist16 = take(sizeof(uint32_t) * 65536);
+  l.h16part = take(sizeof(uint32_t) * 32768 * size_t(H16_MAXCTA));
   l.tasks = take(sizeof(Task) * g.maxtasks);
   l.dtasks = take(g.vb == 0 ? sizeof(DTask) * g.maxtasks : 0);
   l.keys = take(size_t(g.kb) * g.n);
@@ -170,6 +171,7 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   }
   ws.status = reinterpret_cast<uint32_t *>(base + lay.status);
   ws.hist16 = reinterpret_cast<uint32_t *>(base + lay.hist16);
+  ws.h16part = reinterpret_cast<uint32_t *>(base + lay.h16part);
   ws.tasks = reinterpret_cast<Task *>(base + lay.tasks);
   ws.dtasks = reinterpret_cast<DTask *>(base + lay.dtasks);
   ws.keys[0] = keys;
@@ -248,7 +250,11 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   if (n > geo.local_max) {
     const int nlev = geo.ndig + 1;
     for (int L = 0; L < nlev; ++L) {
-      if (L == 0) BS_CUDA(pdl_launch(h16, num_sms(), H16_BLOCK, H16_SMEM, st, ws));
+      if (L == 0) {
+        const int parts = num_sms() < H16_MAXCTA ? num_sms() : H16_MAXCTA;
+        BS_CUDA(pdl_launch(h16, parts, H16_BLOCK, H16_SMEM, st, ws));
+        BS_CUDA(pdl_launch(hist16_reduce_kernel, 32768 / 4 / 64, 256, 0, st, ws, parts));
+      }
       else BS_CUDA(pdl_launch(hk, hk_grid, HI_BLOCK, 0, st, ws, L));
       mark(st);
       BS_CUDA(pdl_launch(plan_kernel<K>, num_sms() * 4, 256, 0, st, ws, L));
@@ -379,7 +385,8 @@ int bs_sort_launches(uint64_t n, int key_bytes, int width, int start_pos, int wi
   if (n <= 1 || width_eff <= 0) return 0;
   const Geometry g = geometry(n, key_bytes, 0, width_eff);
   int k = 3;  // init + dense + local
-  if (n > g.local_max) k += 4 * (g.ndig + 1) + (key_bytes == 4 ? g.ndig : 0);  // + big dense per level
+  // per level hist/plan/scatter/expand (+ big dense), + the level-0 hist16 reduce
+  if (n > g.local_max) k += 4 * (g.ndig + 1) + (key_bytes == 4 ? g.ndig : 0) + 1;
   if (with_counters) k += 2;
   return k;
 }

@@ -105,6 +105,7 @@ struct Ws {
   uint32_t *tile_bucket[2];
   uint32_t *status;  // [maxtiles][256]
   uint32_t *hist16;  // [65536]: root histogram of the digit pair (dig, dig+1)
+  uint32_t *h16part; // [H16_MAXCTA][32768]: per-CTA packed partial rows
   Task *tasks;
   DTask *dtasks;
   int dense;           // keys-only full-width: dense tasks go to dense_kernel
@@ -281,13 +282,14 @@ __global__ void __launch_bounds__(BLOCK) hist_kernel(Ws ws, int L) {
 // K1 at level 0: histogram of the digit PAIR (dig, dig+1) of the root bucket,
 // so the root's 256 children need no histogram pass of their own (plan(0)
 // marks them BK_HKNOWN; expand(1) copies their rows).  One CTA per SM keeps
-// 65536 16-bit bins in 128 KB of shared memory, two per word, each a 15-bit
-// count under a guard bit: the increment that sets a guard bit (old count
-// 0x7FFF) clears it again and moves 32768 to the global counts, so no carry
-// ever crosses into the neighbouring bin and the counts are exact for any
-// input.  Also yields the root's 256-bin histogram (row sums) and OR/AND
+// 65536 16-bit bins in 128 KB of shared memory, two per word; sweeps between
+// epochs of 32768 keys move every half that reached 0x8000 to the global
+// counts, so no carry ever crosses into the neighbouring bin and the counts
+// are exact for any input.  Also yields the root's 256-bin histogram (row sums) and OR/AND
 // masks.
 // ---------------------------------------------------------------------------
+constexpr int H16_MAXCTA = 160;  // >= SM count (one CTA per SM)
+
 template <typename K, int KIND, int BLOCK>
 __global__ void __launch_bounds__(BLOCK, 1) hist16_kernel(Ws ws) {
   pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
@@ -320,18 +322,19 @@ __global__ void __launch_bounds__(BLOCK, 1) hist16_kernel(Ws ws) {
   const uint64_t ng = (uint64_t(head) + n + EPG - 1) / EPG;
   const uint64_t g0 = ng * blockIdx.x / gridDim.x, g1 = ng * (blockIdx.x + 1) / gridDim.x;
   K o = 0, a = ~K(0);
+  // Bin p: count in half (p & 1) of word p >> 1, incremented without a
+  // return value.  Epochs of at most 32768 keys per CTA are separated by a
+  // sweep that moves every half at or above 0x8000 to the global counts, so
+  // no half can exceed 0x7FFF + 32768 = 0xFFFF between sweeps: exact for any
+  // input, with no per-key overflow test.
+  constexpr int GPE = 32768 / (BLOCK * EPG);  // granules per thread per epoch
+  static_assert(GPE % UNR == 0 && GPE > 0, "whole batches per epoch");
   auto count = [&](K x) {
     const K nk = g.norm(x);
     o |= nk;
     a &= nk;
-    const uint32_t p = ((uint32_t(nk >> shA) & msk) << post);
-    const uint32_t sh = (p & 1u) << 4;
-    const uint32_t old = atomicAdd(&hw[p >> 1], 1u << sh);
-    if (((old >> sh) & 0xFFFFu) == 0x7FFFu) {  // guard bit just set: spill 32768
-      atomicSub(&hw[p >> 1], 0x8000u << sh);
-      atomicAdd(&ws.hist16[p], 32768u);
-      atomicAdd(&ws.bhist[0][p >> 8], 32768u);
-    }
+    const uint32_t p = (uint32_t(nk >> shA) & msk) << post;
+    atomicAdd(&hw[p >> 1], 1u + (p & 1u) * 0xFFFFu);
   };
   auto granule = [&](uint64_t gi, const uint4 &v) {
     K kk[EPG];
@@ -351,27 +354,48 @@ __global__ void __launch_bounds__(BLOCK, 1) hist16_kernel(Ws ws) {
         if (e0 + j >= 0 && e0 + j < int64_t(n)) count(kk[j]);
     }
   };
-  uint64_t gi = g0 + tid;
-  for (; gi + uint64_t(UNR - 1) * BLOCK < g1; gi += uint64_t(UNR) * BLOCK) {
-    uint4 v[UNR];
+  for (uint64_t eb = g0; eb < g1; eb += uint64_t(GPE) * BLOCK) {  // block-uniform epochs
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) v[u] = __ldcs(gsrc + gi + uint64_t(u) * BLOCK);
+    for (int u0 = 0; u0 < GPE; u0 += UNR) {
+      uint4 v[UNR];
 #pragma unroll
-    for (int u = 0; u < UNR; ++u) granule(gi + uint64_t(u) * BLOCK, v[u]);
-  }
-  for (; gi < g1; gi += BLOCK) granule(gi, __ldcs(gsrc + gi));
-  __syncthreads();
-  // flush: nonzero pair bins to hist16, row sums to the root's histogram
-  for (int i = tid; i < 32768; i += BLOCK) {
-    const uint32_t v = hw[i], lo = v & 0xFFFFu, hi = v >> 16;
-    if (two) {
-      if (lo) atomicAdd(&ws.hist16[2 * i], lo);
-      if (hi) atomicAdd(&ws.hist16[2 * i + 1], hi);
+      for (int u = 0; u < UNR; ++u) {
+        const uint64_t gi = eb + uint64_t(u0 + u) * BLOCK + tid;
+        v[u] = gi < g1 ? __ldcs(gsrc + gi) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const uint64_t gi = eb + uint64_t(u0 + u) * BLOCK + tid;
+        if (gi < g1) granule(gi, v[u]);
+      }
     }
-    uint32_t sum = lo + hi;
+    __syncthreads();
+    for (int q = tid; q < 32768 / 4; q += BLOCK) {  // sweep (rarely finds anything)
+      uint4 wv = reinterpret_cast<const uint4 *>(hw)[q];
+      if ((wv.x | wv.y | wv.z | wv.w) & 0x80008000u) {
+        uint32_t *ww = &wv.x;
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, off);
-    if (lane == 0 && sum) atomicAdd(&ws.bhist[0][i >> 7], sum);  // 128 words per digit
+        for (int k = 0; k < 4; ++k) {
+          for (int h = 0; h < 2; ++h) {
+            if (ww[k] & (0x8000u << (16 * h))) {
+              const uint32_t p = 2u * (4u * q + k) + h;
+              atomicAdd(&ws.hist16[p], 32768u);
+              atomicAdd(&ws.bhist[0][p >> 8], 32768u);
+            }
+          }
+          ww[k] &= 0x7FFF7FFFu;
+        }
+        reinterpret_cast<uint4 *>(hw)[q] = wv;
+      }
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  // flush: this CTA's packed bins to its partial row (plain coalesced stores;
+  // hist16_reduce_kernel folds the rows)
+  {
+    uint4 *dst = reinterpret_cast<uint4 *>(ws.h16part + size_t(blockIdx.x) * 32768);
+    for (int q = tid; q < 32768 / 4; q += BLOCK) dst[q] = reinterpret_cast<const uint4 *>(hw)[q];
   }
   const K oo = warp_or(o), aa = warp_and(a);
   if (lane == 0) {
@@ -389,6 +413,53 @@ __global__ void __launch_bounds__(BLOCK, 1) hist16_kernel(Ws ws) {
     atomicAnd(reinterpret_cast<unsigned long long *>(&ws.band[0][0]),
               (unsigned long long)(uint64_t(y) | (sizeof(K) == 4 ? 0xFFFFFFFF00000000ull : 0ull)));
   }
+}
+
+// Fold hist16_kernel's per-CTA partial rows (two u16 bins per word) into
+// hist16 (which already holds the sweeps' spills) and the root's 256-bin
+// histogram.  Thread (quad q, slice k) sums word quad q over a quarter of the
+// rows; the four slices meet in shared memory.  256 threads = 64 quads.
+__global__ void __launch_bounds__(256) hist16_reduce_kernel(Ws ws, int nparts) {
+  pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
+  __shared__ uint4 s_part[3][64][2];  // slices 1..3: (lo sums, hi sums) of 4 words
+  if (ws.ctl->nbuckets[0] == 0) return;
+  const int tid = threadIdx.x, ql = tid & 63, k = tid >> 6;
+  const uint32_t q = blockIdx.x * 64u + uint32_t(ql);  // word quad: bins 8q .. 8q+7
+  const uint4 *src = reinterpret_cast<const uint4 *>(ws.h16part);
+  uint4 lo = make_uint4(0, 0, 0, 0), hi = make_uint4(0, 0, 0, 0);
+  const int p0 = nparts * k / 4, p1 = nparts * (k + 1) / 4;
+#pragma unroll 4
+  for (int pp = p0; pp < p1; ++pp) {
+    const uint4 v = src[size_t(pp) * 8192 + q];
+    lo.x += v.x & 0xFFFFu, hi.x += v.x >> 16;
+    lo.y += v.y & 0xFFFFu, hi.y += v.y >> 16;
+    lo.z += v.z & 0xFFFFu, hi.z += v.z >> 16;
+    lo.w += v.w & 0xFFFFu, hi.w += v.w >> 16;
+  }
+  if (k > 0) {
+    s_part[k - 1][ql][0] = lo;
+    s_part[k - 1][ql][1] = hi;
+  }
+  __syncthreads();
+  if (k != 0) return;
+  for (int j = 0; j < 3; ++j) {
+    const uint4 l = s_part[j][ql][0], h = s_part[j][ql][1];
+    lo.x += l.x, lo.y += l.y, lo.z += l.z, lo.w += l.w;
+    hi.x += h.x, hi.y += h.y, hi.z += h.z, hi.w += h.w;
+  }
+  if (ws.ctl->h16_bad == 0u) {
+    uint4 *h0 = reinterpret_cast<uint4 *>(ws.hist16) + 2 * q;  // bins 8q..8q+3, 8q+4..8q+7
+    uint4 a0 = h0[0], a1 = h0[1];
+    a0.x += lo.x, a0.y += hi.x, a0.z += lo.y, a0.w += hi.y;
+    a1.x += lo.z, a1.y += hi.z, a1.z += lo.w, a1.w += hi.w;
+    h0[0] = a0;
+    h0[1] = a1;
+  }
+  // 32 quads (one warp's lanes 0..31 of a slice-0 half) = 256 bins = one row
+  uint32_t sum = lo.x + lo.y + lo.z + lo.w + hi.x + hi.y + hi.z + hi.w;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, off);
+  if ((tid & 31) == 0 && sum) atomicAdd(&ws.bhist[0][q >> 5], sum);
 }
 
 // ---------------------------------------------------------------------------
