@@ -88,6 +88,20 @@ int bs_sort_profiled(void *keys, void *vals, uint64_t n, int key_bytes,
                      void *ws, size_t ws_bytes, void *stream, int64_t *counters,
                      int64_t depth, float *phase_ms, int nphases, int *nrecorded);
 
+/*
+ * bs_sort from a separate source: sorts src_keys[0..n) (+src_vals) into
+ * keys[0..n) (+vals), using the source buffers as the MSD ping-pong copy (their
+ * contents are destroyed).  Same order, stability and arguments as bs_sort;
+ * ws must hold bs_sort_from_workspace_bytes(n, ...), which has no n-element
+ * copy.  The multi-GPU front end sorts each rank's receive buffer this way
+ * (the receive buffer stays registered for peer access; the result lands in
+ * a fresh caller buffer).  Replaces the local sort after the exchange in
+ * variants.sort_parallel (variants.py:195-206).
+ */
+size_t bs_sort_from_workspace_bytes(uint64_t n, int key_bytes, int val_bytes);
+int bs_sort_from(void *src_keys, void *src_vals, void *keys, void *vals, uint64_t n,
+                 int key_bytes, int val_bytes, int width, int start_pos,
+                 int key_kind, void *ws, size_t ws_bytes, void *stream);
 /* Number of kernels bs_sort launches for this shape (for launch accounting). */
 int bs_sort_launches(uint64_t n, int key_bytes, int width, int start_pos,
                      int with_counters);
@@ -148,6 +162,44 @@ int bs_split_by_splitters(const void *keys, const void *vals, uint64_t n,
                           void *out_keys, void *out_vals, uint64_t *class_counts,
                           void *ws, size_t ws_bytes, void *stream);
 
+/*
+ * Fused destination partition + exchange over peer memory (one kernel instead
+ * of partition -> ncclAllToAllv):
+ *   bs_split_count: per-tile class histogram and class-major scan of keys
+ *     against the splitters (as bs_split_by_splitters); writes the 2R-1 class
+ *     counts (device uint64) and keeps the tile offsets in ws for
+ *   bs_split_exchange: with delta[c] = (global class-major position of this
+ *     rank's first class-c element) - (its shard-local class-major position)
+ *     and bounds[0..R] (destination d owns global positions [bounds[d],
+ *     bounds[d+1])), stores every element at dst_keys[d][gpos - bounds[d]]
+ *     (dst_vals alike).  dst_keys / dst_vals are DEVICE arrays of R device
+ *     pointers, normally peer mappings of the other ranks' receive buffers
+ *     (bs_ipc_open).  Call with the same ws right after bs_split_count on the
+ *     same keys.  The grid ends with a system-scope fence; the caller orders
+ *     the receivers after it (stream order + a collective).
+ * delta: device int64[2R-1]; bounds: device uint64[R+1].
+ */
+int bs_split_count(const void *keys, uint64_t n, int key_bytes, int width,
+                   int key_kind, const void *splitters, int nranks,
+                   uint64_t *class_counts, void *ws, size_t ws_bytes, void *stream);
+int bs_split_exchange(const void *keys, const void *vals, uint64_t n,
+                      int key_bytes, int val_bytes, int width, int key_kind,
+                      const void *splitters, int nranks, const int64_t *delta,
+                      const uint64_t *bounds, void *const *dst_keys,
+                      void *const *dst_vals, void *ws, size_t ws_bytes,
+                      void *stream);
+/*
+ * Peer-mapped receive buffers (CUDA IPC; one process per GPU on an
+ * NVLink/NVSwitch node).  bs_ipc_alloc allocates `bytes` of device memory and
+ * writes its export handle (bs_ipc_handle_bytes() bytes) to `handle`;
+ * bs_ipc_open maps another process's handle (peer access enabled lazily);
+ * bs_ipc_close unmaps; bs_ipc_free releases an allocation of this process.
+ */
+size_t bs_ipc_handle_bytes(void);
+int bs_ipc_alloc(size_t bytes, void **ptr, void *handle);
+int bs_ipc_open(const void *handle, void **ptr);
+int bs_ipc_close(void *ptr);
+int bs_ipc_free(void *ptr);
 /*
  * Gather `count` uniformly strided samples of the encoded, normalised sort key
  * (device, key_bytes words) from keys[0..n): sample i is element

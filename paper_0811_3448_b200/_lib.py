@@ -33,6 +33,8 @@ EXPORTS = (
     "bs_metrics_workspace_bytes", "bs_metrics", "bs_partition_workspace_bytes",
     "bs_partition_words", "bs_range_sorted", "bs_split_workspace_bytes",
     "bs_split_by_splitters", "bs_sample_keys", "bs_sort_profiled", "bs_sort_launches",
+    "bs_sort_from_workspace_bytes", "bs_sort_from", "bs_split_count", "bs_split_exchange",
+    "bs_ipc_handle_bytes", "bs_ipc_alloc", "bs_ipc_open", "bs_ipc_close", "bs_ipc_free",
 )
 
 
@@ -105,6 +107,23 @@ def lib() -> ctypes.CDLL:
         L.bs_sort_profiled.restype = i32
         L.bs_sort_launches.argtypes = [u64, i32, i32, i32, i32]
         L.bs_sort_launches.restype = i32
+        L.bs_sort_from_workspace_bytes.argtypes = [u64, i32, i32]
+        L.bs_sort_from_workspace_bytes.restype = sz
+        L.bs_sort_from.argtypes = [vp, vp, vp, vp, u64, i32, i32, i32, i32, i32, vp, sz, vp]
+        L.bs_sort_from.restype = i32
+        L.bs_split_count.argtypes = [vp, u64, i32, i32, i32, vp, i32, vp, vp, sz, vp]
+        L.bs_split_count.restype = i32
+        L.bs_split_exchange.argtypes = [vp, vp, u64, i32, i32, i32, i32, vp, i32, vp, vp, vp, vp, vp, sz, vp]
+        L.bs_split_exchange.restype = i32
+        L.bs_ipc_handle_bytes.restype = sz
+        L.bs_ipc_alloc.argtypes = [sz, ctypes.POINTER(vp), vp]
+        L.bs_ipc_alloc.restype = i32
+        L.bs_ipc_open.argtypes = [vp, ctypes.POINTER(vp)]
+        L.bs_ipc_open.restype = i32
+        L.bs_ipc_close.argtypes = [vp]
+        L.bs_ipc_close.restype = i32
+        L.bs_ipc_free.argtypes = [vp]
+        L.bs_ipc_free.restype = i32
         _lib = L
         return L
 

@@ -116,7 +116,7 @@ struct Layout {
   size_t ctl, buckets[2], bhist[2], bor[2], band[2], tile_bucket[2], status, hist16, h16part, tasks, dtasks, keys, vals, total;
 };
 
-static Layout layout(const Geometry &g) {
+static Layout layout(const Geometry &g, bool own_copy = true) {
   Layout l{};
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -137,8 +137,9 @@ static Layout layout(const Geometry &g) {
   l.h16part = take(sizeof(uint32_t) * 32768 * size_t(H16_MAXCTA));
   l.tasks = take(sizeof(Task) * g.maxtasks);
   l.dtasks = take(g.vb == 0 ? sizeof(DTask) * g.maxtasks : 0);
-  l.keys = take(size_t(g.kb) * g.n);
-  l.vals = take(size_t(g.vb) * g.n);
+  // the ping-pong copy (bs_sort_from uses the caller's source buffer instead)
+  l.keys = take(own_copy ? size_t(g.kb) * g.n : 0);
+  l.vals = take(own_copy ? size_t(g.vb) * g.n : 0);
   l.total = off;
   return l;
 }
@@ -152,10 +153,10 @@ static int max_active(F kernel, int block, size_t smem) {
 
 template <typename K, int VB, int KIND>
 static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp, size_t ws_bytes,
-                    cudaStream_t st) {
+                    cudaStream_t st, void *src_keys = nullptr, void *src_vals = nullptr) {
   const int kb = int(sizeof(K));
   const Geometry geo = geometry(n, kb, VB, width_eff);
-  const Layout lay = layout(geo);
+  const Layout lay = layout(geo, src_keys == nullptr);
   if (ws_bytes < lay.total)
     return fail(BS_ERR_WORKSPACE, "workspace too small: need " + std::to_string(lay.total) +
                                       " bytes, got " + std::to_string(ws_bytes));
@@ -175,9 +176,10 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   ws.tasks = reinterpret_cast<Task *>(base + lay.tasks);
   ws.dtasks = reinterpret_cast<DTask *>(base + lay.dtasks);
   ws.keys[0] = keys;
-  ws.keys[1] = base + lay.keys;
+  ws.keys[1] = src_keys ? src_keys : base + lay.keys;
   ws.vals[0] = vals;
-  ws.vals[1] = VB ? base + lay.vals : nullptr;
+  ws.vals[1] = VB ? (src_keys ? src_vals : base + lay.vals) : nullptr;
+  ws.root_parity = src_keys ? 1u : 0u;
   ws.n = n;
   ws.maxb = geo.maxb;
   ws.maxtiles = geo.maxtiles;
@@ -355,6 +357,46 @@ int bs_sort(void *keys, void *vals, uint64_t n, int key_bytes, int val_bytes, in
   return BS_OK;
 }
 
+size_t bs_sort_from_workspace_bytes(uint64_t n, int key_bytes, int val_bytes) {
+  if ((key_bytes != 4 && key_bytes != 8) || (val_bytes != 0 && val_bytes != 4 && val_bytes != 8)) return 0;
+  return layout(geometry(n, key_bytes, val_bytes, key_bytes * 8), false).total;
+}
+
+int bs_sort_from(void *src_keys, void *src_vals, void *keys, void *vals, uint64_t n, int key_bytes, int val_bytes,
+                 int width, int start_pos, int key_kind, void *ws, size_t ws_bytes, void *stream) {
+  int rc = check_common(key_bytes, val_bytes, width, start_pos, key_kind);
+  if (rc) return rc;
+  if (n >= (uint64_t(1) << 30) + 1) return fail(BS_ERR_VALUE, "n > 2^30 elements per call is not supported");
+  if (n > 0 && (src_keys == nullptr || keys == nullptr)) return fail(BS_ERR_VALUE, "NULL key buffer");
+  if (val_bytes != 0 && n > 0 && (src_vals == nullptr || vals == nullptr))
+    return fail(BS_ERR_VALUE, "val_bytes > 0 but a value buffer is NULL");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int width_eff = width - start_pos;
+  if (key_kind == BS_KEY_SIGNED && start_pos > 0) key_kind = BS_KEY_UNSIGNED;
+  if (n <= 1 || width_eff == 0) {  // nothing to order: the result is the source
+    if (n) BS_CUDA(cudaMemcpyAsync(keys, src_keys, n * key_bytes, cudaMemcpyDeviceToDevice, st));
+    if (n && val_bytes) BS_CUDA(cudaMemcpyAsync(vals, src_vals, n * val_bytes, cudaMemcpyDeviceToDevice, st));
+    return BS_OK;
+  }
+  if (val_bytes == 0) vals = src_vals = nullptr;
+#define BS_DISPATCH_F(K, KIND)                                                                             \
+  do {                                                                                                     \
+    if (val_bytes == 0) rc = run_sort<K, 0, KIND>(keys, vals, n, width_eff, ws, ws_bytes, st, src_keys, src_vals); \
+    else if (val_bytes == 4) rc = run_sort<K, 4, KIND>(keys, vals, n, width_eff, ws, ws_bytes, st, src_keys, src_vals); \
+    else rc = run_sort<K, 8, KIND>(keys, vals, n, width_eff, ws, ws_bytes, st, src_keys, src_vals);      \
+  } while (0)
+  if (key_bytes == 4) {
+    if (key_kind == BS_KEY_UNSIGNED) BS_DISPATCH_F(uint32_t, 0);
+    else BS_DISPATCH_F(uint32_t, 1);
+  } else {
+    if (key_kind == BS_KEY_UNSIGNED) BS_DISPATCH_F(uint64_t, 0);
+    else if (key_kind == BS_KEY_SIGNED) BS_DISPATCH_F(uint64_t, 1);
+    else BS_DISPATCH_F(uint64_t, 2);
+  }
+#undef BS_DISPATCH_F
+  return rc;
+}
+
 int bs_sort_profiled(void *keys, void *vals, uint64_t n, int key_bytes, int val_bytes, int width, int start_pos,
                      int key_kind, void *ws, size_t ws_bytes, void *stream, int64_t *counters, int64_t depth,
                      float *phase_ms, int nphases, int *nrecorded) {
@@ -486,38 +528,17 @@ int bs_range_sorted(const void *keys, uint64_t n, int key_bytes, void *stream, i
 
 size_t bs_split_workspace_bytes(uint64_t n, int, int, int) {
   const uint64_t ntiles = (n + SPLIT_TILE - 1) / SPLIT_TILE;
-  return align_up(sizeof(uint32_t) * 16 * (ntiles + 1));
+  const uint64_t nchunks = (ntiles + SCAN_CHUNK - 1) / SCAN_CHUNK;
+  return align_up(sizeof(uint32_t) * 16 * (ntiles + 1)) + align_up(sizeof(uint32_t) * 16 * (nchunks + 1)) +
+         align_up(sizeof(uint32_t) * 16);
 }
 
-int bs_split_by_splitters(const void *keys, const void *vals, uint64_t n, int key_bytes, int val_bytes,
-                          int width, int key_kind, const void *splitters, int nranks, void *out_keys,
-                          void *out_vals, uint64_t *class_counts, void *ws, size_t ws_bytes, void *stream) {
-  int rc = check_common(key_bytes, val_bytes, width, 0, key_kind);
-  if (rc) return rc;
-  if (nranks < 1 || nranks > 8) return fail(BS_ERR_VALUE, "nranks must be in [1, 8]");
-  if (n >= (uint64_t(1) << 32)) return fail(BS_ERR_VALUE, "n too large");
-  if (ws_bytes < bs_split_workspace_bytes(n, key_bytes, val_bytes, nranks))
-    return fail(BS_ERR_WORKSPACE, "workspace too small");
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int ncls = 2 * nranks - 1, nsp = nranks - 1;
-  BS_CUDA(cudaMemsetAsync(class_counts, 0, sizeof(uint64_t) * ncls, st));
-  if (n == 0) return BS_OK;
-  const uint32_t ntiles = uint32_t((n + SPLIT_TILE - 1) / SPLIT_TILE);
-  uint32_t *tile_hist = static_cast<uint32_t *>(ws);
-  const int shift0 = key_bytes * 8 - width;
-  auto go = [&](auto ktag, auto kindc, auto vbc) -> int {
-    using K = decltype(ktag);
-    constexpr int KIND = decltype(kindc)::value;
-    constexpr int VB = decltype(vbc)::value;
-    split_hist_kernel<K, KIND><<<ntiles, SPLIT_BLOCK, 0, st>>>(static_cast<const K *>(keys), n, shift0,
-                                                               static_cast<const K *>(splitters), nsp, tile_hist);
-    split_scan_kernel<<<1, 32, 0, st>>>(tile_hist, ntiles, ncls, reinterpret_cast<unsigned long long *>(class_counts));
-    split_scatter_kernel<K, VB, KIND><<<ntiles, SPLIT_BLOCK, 0, st>>>(
-        static_cast<const K *>(keys), vals, n, shift0, static_cast<const K *>(splitters), nsp, tile_hist,
-        static_cast<K *>(out_keys), out_vals);
-    BS_CUDA(cudaGetLastError());
-    return BS_OK;
-  };
+}  // extern "C"
+
+namespace bs {
+
+template <typename F>
+static int split_dispatch(int key_bytes, int key_kind, int val_bytes, F &&go) {
   using I0 = std::integral_constant<int, 0>;
   using I1 = std::integral_constant<int, 1>;
   using I2 = std::integral_constant<int, 2>;
@@ -532,6 +553,155 @@ int bs_split_by_splitters(const void *keys, const void *vals, uint64_t n, int ke
   if (key_kind == 0) return by_v(uint64_t(0), I0{});
   if (key_kind == 1) return by_v(uint64_t(0), I1{});
   return by_v(uint64_t(0), I2{});
+}
+
+struct SplitWs {
+  uint32_t *tile_hist, *chunk_sum, *class_base;
+  uint32_t ntiles, nchunks;
+};
+
+static SplitWs split_ws(void *ws, uint64_t n) {
+  SplitWs w{};
+  w.ntiles = uint32_t((n + SPLIT_TILE - 1) / SPLIT_TILE);
+  w.nchunks = (w.ntiles + SCAN_CHUNK - 1) / SCAN_CHUNK;
+  char *b = static_cast<char *>(ws);
+  w.tile_hist = reinterpret_cast<uint32_t *>(b);
+  b += align_up(sizeof(uint32_t) * 16 * (uint64_t(w.ntiles) + 1));
+  w.chunk_sum = reinterpret_cast<uint32_t *>(b);
+  b += align_up(sizeof(uint32_t) * 16 * (uint64_t(w.nchunks) + 1));
+  w.class_base = reinterpret_cast<uint32_t *>(b);
+  return w;
+}
+
+static int split_check(uint64_t n, int key_bytes, int val_bytes, int width, int key_kind, int nranks,
+                       size_t ws_bytes) {
+  int rc = check_common(key_bytes, val_bytes, width, 0, key_kind);
+  if (rc) return rc;
+  if (nranks < 1 || nranks > 8) return fail(BS_ERR_VALUE, "nranks must be in [1, 8]");
+  if (n >= (uint64_t(1) << 32)) return fail(BS_ERR_VALUE, "n too large");
+  if (ws_bytes < bs_split_workspace_bytes(n, key_bytes, val_bytes, nranks))
+    return fail(BS_ERR_WORKSPACE, "workspace too small");
+  return BS_OK;
+}
+
+// class histogram per tile + parallel class-major scan (tile offsets stay in ws)
+static int split_count(const void *keys, uint64_t n, int key_bytes, int width, int key_kind, const void *splitters,
+                       int nranks, uint64_t *class_counts, void *ws, cudaStream_t st) {
+  const int ncls = 2 * nranks - 1, nsp = nranks - 1;
+  BS_CUDA(cudaMemsetAsync(class_counts, 0, sizeof(uint64_t) * ncls, st));
+  if (n == 0) return BS_OK;
+  const SplitWs w = split_ws(ws, n);
+  const int shift0 = key_bytes * 8 - width;
+  return split_dispatch(key_bytes, key_kind, 0, [&](auto ktag, auto kindc, auto) -> int {
+    using K = decltype(ktag);
+    constexpr int KIND = decltype(kindc)::value;
+    split_hist_kernel<K, KIND><<<w.ntiles, SPLIT_BLOCK, 0, st>>>(static_cast<const K *>(keys), n, shift0,
+                                                                 static_cast<const K *>(splitters), nsp, w.tile_hist);
+    split_chunk_sum_kernel<<<w.nchunks, 256, 0, st>>>(w.tile_hist, w.ntiles, w.chunk_sum);
+    split_top_scan_kernel<<<1, 512, 0, st>>>(w.chunk_sum, w.nchunks, ncls,
+                                             reinterpret_cast<unsigned long long *>(class_counts), w.class_base);
+    split_chunk_scan_kernel<<<w.nchunks, 256, 0, st>>>(w.tile_hist, w.ntiles, w.chunk_sum, w.class_base);
+    BS_CUDA(cudaGetLastError());
+    return BS_OK;
+  });
+}
+
+}  // namespace bs
+
+extern "C" {
+
+int bs_split_by_splitters(const void *keys, const void *vals, uint64_t n, int key_bytes, int val_bytes,
+                          int width, int key_kind, const void *splitters, int nranks, void *out_keys,
+                          void *out_vals, uint64_t *class_counts, void *ws, size_t ws_bytes, void *stream) {
+  int rc = split_check(n, key_bytes, val_bytes, width, key_kind, nranks, ws_bytes);
+  if (rc) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  rc = split_count(keys, n, key_bytes, width, key_kind, splitters, nranks, class_counts, ws, st);
+  if (rc || n == 0) return rc;
+  const SplitWs w = split_ws(ws, n);
+  const int shift0 = key_bytes * 8 - width, nsp = nranks - 1;
+  return split_dispatch(key_bytes, key_kind, val_bytes, [&](auto ktag, auto kindc, auto vbc) -> int {
+    using K = decltype(ktag);
+    constexpr int KIND = decltype(kindc)::value;
+    constexpr int VB = decltype(vbc)::value;
+    split_scatter_kernel<K, VB, KIND><<<w.ntiles, SPLIT_BLOCK, 0, st>>>(
+        static_cast<const K *>(keys), vals, n, shift0, static_cast<const K *>(splitters), nsp, w.tile_hist,
+        static_cast<K *>(out_keys), out_vals);
+    BS_CUDA(cudaGetLastError());
+    return BS_OK;
+  });
+}
+
+int bs_split_count(const void *keys, uint64_t n, int key_bytes, int width, int key_kind, const void *splitters,
+                   int nranks, uint64_t *class_counts, void *ws, size_t ws_bytes, void *stream) {
+  int rc = split_check(n, key_bytes, 0, width, key_kind, nranks, ws_bytes);
+  if (rc) return rc;
+  return split_count(keys, n, key_bytes, width, key_kind, splitters, nranks, class_counts, ws,
+                     static_cast<cudaStream_t>(stream));
+}
+
+int bs_split_exchange(const void *keys, const void *vals, uint64_t n, int key_bytes, int val_bytes, int width,
+                      int key_kind, const void *splitters, int nranks, const int64_t *delta,
+                      const uint64_t *bounds, void *const *dst_keys, void *const *dst_vals, void *ws,
+                      size_t ws_bytes, void *stream) {
+  int rc = split_check(n, key_bytes, val_bytes, width, key_kind, nranks, ws_bytes);
+  if (rc) return rc;
+  if (val_bytes != 0 && (vals == nullptr || dst_vals == nullptr))
+    return fail(BS_ERR_VALUE, "val_bytes > 0 but vals or dst_vals is NULL");
+  if (n == 0) return BS_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const SplitWs w = split_ws(ws, n);
+  const int shift0 = key_bytes * 8 - width, nsp = nranks - 1;
+  return split_dispatch(key_bytes, key_kind, val_bytes, [&](auto ktag, auto kindc, auto vbc) -> int {
+    using K = decltype(ktag);
+    constexpr int KIND = decltype(kindc)::value;
+    constexpr int VB = decltype(vbc)::value;
+    auto kern = split_exchange_kernel<K, VB, KIND>;
+    const size_t smem = ExchangeSmem<K, VB>::bytes;
+    BS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    kern<<<w.ntiles, SPLIT_BLOCK, smem, st>>>(static_cast<const K *>(keys), vals, n, shift0,
+                                              static_cast<const K *>(splitters), nsp, w.tile_hist,
+                                              reinterpret_cast<const long long *>(delta),
+                                              reinterpret_cast<const unsigned long long *>(bounds), nranks,
+                                              reinterpret_cast<K *const *>(dst_keys), dst_vals);
+    BS_CUDA(cudaGetLastError());
+    return BS_OK;
+  });
+}
+
+size_t bs_ipc_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
+
+int bs_ipc_alloc(size_t bytes, void **ptr, void *handle) {
+  if (!ptr || !handle) return fail(BS_ERR_VALUE, "ptr and handle must be non-NULL");
+  *ptr = nullptr;
+  BS_CUDA(cudaMalloc(ptr, bytes ? bytes : 1));
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, *ptr);
+  if (e != cudaSuccess) {
+    cudaFree(*ptr);
+    *ptr = nullptr;
+    return fail(BS_ERR_CUDA, std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
+  }
+  std::memcpy(handle, &h, sizeof(h));
+  return BS_OK;
+}
+
+int bs_ipc_open(const void *handle, void **ptr) {
+  if (!ptr || !handle) return fail(BS_ERR_VALUE, "ptr and handle must be non-NULL");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  BS_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return BS_OK;
+}
+
+int bs_ipc_close(void *ptr) {
+  BS_CUDA(cudaIpcCloseMemHandle(ptr));
+  return BS_OK;
+}
+
+int bs_ipc_free(void *ptr) {
+  BS_CUDA(cudaFree(ptr));
+  return BS_OK;
 }
 
 int bs_sample_keys(const void *keys, uint64_t n, int key_bytes, int width, int key_kind, uint64_t count,

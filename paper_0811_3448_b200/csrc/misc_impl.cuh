@@ -242,30 +242,6 @@ __global__ void split_hist_kernel(const K *keys, uint64_t n, int shift0, const K
   if (threadIdx.x < 16) tile_hist[size_t(blockIdx.x) * 16 + threadIdx.x] = h[threadIdx.x];
 }
 
-// one CTA: class-major exclusive scan over (class, tile) -> absolute offsets
-__global__ void split_scan_kernel(uint32_t *tile_hist, uint32_t ntiles, int ncls,
-                                  unsigned long long *class_counts) {
-  __shared__ unsigned long long tot[16];
-  const int c = threadIdx.x;
-  if (c < 16) {
-    unsigned long long s = 0;
-    if (c < ncls)
-      for (uint32_t t = 0; t < ntiles; ++t) s += tile_hist[size_t(t) * 16 + c];
-    tot[c] = s;
-  }
-  __syncthreads();
-  if (c < ncls) {
-    unsigned long long base = 0;
-    for (int i = 0; i < c; ++i) base += tot[i];
-    for (uint32_t t = 0; t < ntiles; ++t) {
-      const uint32_t v = tile_hist[size_t(t) * 16 + c];
-      tile_hist[size_t(t) * 16 + c] = uint32_t(base);
-      base += v;
-    }
-    class_counts[c] = tot[c];
-  }
-}
-
 template <typename K, int VB, int KIND>
 __global__ void __launch_bounds__(SPLIT_BLOCK) split_scatter_kernel(
     const K *keys, const void *vals_, uint64_t n, int shift0, const K *spl, int nsp,
@@ -327,6 +303,270 @@ __global__ void __launch_bounds__(SPLIT_BLOCK) split_scatter_kernel(
       if constexpr (VB != 0) out_vals[o] = v[j];
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Parallel class-major scan of the per-tile class counts (replaces a serial
+// one-warp walk over all tiles): chunk sums -> one CTA scans the chunk sums
+// per class -> every chunk scans its own tiles.  tile_hist[t][c] becomes the
+// shard-local position of tile t's first class-c element in the class-major
+// order (class bases included).
+// ---------------------------------------------------------------------------
+constexpr int SCAN_TPT = 4;                      // tiles per thread
+constexpr int SCAN_CHUNK = SCAN_TPT * 256;       // tiles per chunk (256-thread CTAs)
+
+__device__ __forceinline__ void load_row16(const uint32_t *row, uint32_t (&c)[16]) {
+  const uint4 *r = reinterpret_cast<const uint4 *>(row);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint4 v = r[q];
+    c[4 * q] = v.x, c[4 * q + 1] = v.y, c[4 * q + 2] = v.z, c[4 * q + 3] = v.w;
+  }
+}
+
+__global__ void __launch_bounds__(256) split_chunk_sum_kernel(const uint32_t *tile_hist, uint32_t ntiles,
+                                                              uint32_t *chunk_sum /* [nchunks][16] */) {
+  __shared__ uint32_t s[8][16];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  uint32_t acc[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) acc[c] = 0;
+  const uint32_t t0 = blockIdx.x * SCAN_CHUNK + uint32_t(tid) * SCAN_TPT;
+#pragma unroll
+  for (int k = 0; k < SCAN_TPT; ++k) {
+    if (t0 + k < ntiles) {
+      uint32_t c[16];
+      load_row16(tile_hist + size_t(t0 + k) * 16, c);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) acc[q] += c[q];
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    uint32_t v = acc[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    if (lane == 0) s[w][c] = v;
+  }
+  __syncthreads();
+  if (tid < 16) {
+    uint32_t v = 0;
+    for (int i = 0; i < 8; ++i) v += s[i][tid];
+    chunk_sum[size_t(blockIdx.x) * 16 + tid] = v;
+  }
+}
+
+// one CTA of 16 warps: warp c scans class c over the chunks (in place ->
+// exclusive in-class chunk bases); then class bases (class-major) and totals
+__global__ void __launch_bounds__(512) split_top_scan_kernel(uint32_t *chunk_sum, uint32_t nchunks, int ncls,
+                                                             unsigned long long *class_counts,
+                                                             uint32_t *class_base /* [16] */) {
+  __shared__ uint32_t tot[16];
+  const int lane = threadIdx.x & 31, c = threadIdx.x >> 5;
+  uint32_t run = 0;
+  for (uint32_t i0 = 0; i0 < nchunks; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const uint32_t v = i < nchunks ? chunk_sum[size_t(i) * 16 + c] : 0u;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (i < nchunks) chunk_sum[size_t(i) * 16 + c] = run + incl - v;
+    run += __shfl_sync(0xFFFFFFFFu, incl, 31);
+  }
+  if (lane == 0) tot[c] = run;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t b = 0;
+    for (int k = 0; k < 16; ++k) {
+      class_base[k] = b;
+      if (k < ncls) class_counts[k] = tot[k];
+      b += tot[k];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) split_chunk_scan_kernel(uint32_t *tile_hist, uint32_t ntiles,
+                                                               const uint32_t *chunk_sum,
+                                                               const uint32_t *class_base) {
+  __shared__ uint32_t s[8][16];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t t0 = blockIdx.x * SCAN_CHUNK + uint32_t(tid) * SCAN_TPT;
+  uint32_t acc[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) acc[c] = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_TPT; ++k) {
+    if (t0 + k < ntiles) {
+      uint32_t c[16];
+      load_row16(tile_hist + size_t(t0 + k) * 16, c);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) acc[q] += c[q];
+    }
+  }
+  uint32_t ex[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    uint32_t incl = acc[c];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    ex[c] = incl - acc[c];
+    if (lane == 31) s[w][c] = incl;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    uint32_t b = class_base[c] + chunk_sum[size_t(blockIdx.x) * 16 + c];
+    for (int i = 0; i < w; ++i) b += s[i][c];
+    ex[c] += b;
+  }
+#pragma unroll
+  for (int k = 0; k < SCAN_TPT; ++k) {
+    if (t0 + k < ntiles) {
+      uint32_t c[16];
+      uint32_t *row = tile_hist + size_t(t0 + k) * 16;
+      load_row16(row, c);
+      uint4 *r = reinterpret_cast<uint4 *>(row);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        r[q] = make_uint4(ex[4 * q], ex[4 * q + 1], ex[4 * q + 2], ex[4 * q + 3]);
+        ex[4 * q] += c[4 * q], ex[4 * q + 1] += c[4 * q + 1], ex[4 * q + 2] += c[4 * q + 2],
+            ex[4 * q + 3] += c[4 * q + 3];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fused destination partition + exchange (the all-to-all-v of SURVEY §8e
+// step 4 folded into the partition of step 2).  Every element's position in
+// the GLOBAL class-major order is known once the class counts of all ranks
+// are (gpos = shard-local class-major position + delta[class], delta from the
+// host); destination rank d owns global positions [bounds[d], bounds[d+1]),
+// so the element is stored straight into d's receive buffer at
+// gpos - bounds[d] -- a peer (NVLink / NVSwitch) store for d != this rank.
+// A tile is staged in shared memory in class order first, so consecutive
+// threads store consecutive addresses of each class run.  Stable: a class's
+// elements keep shard order, and ranks' blocks are in rank order (delta).
+// ---------------------------------------------------------------------------
+template <typename K, int VB>
+struct ExchangeSmem {
+  using V = typename ValT<VB>::T;
+  static constexpr size_t keys_off = 0;
+  static constexpr size_t vals_off = sizeof(K) * SPLIT_TILE;
+  static constexpr size_t bytes = vals_off + (VB ? sizeof(V) * SPLIT_TILE : 0);
+};
+
+template <typename K, int VB, int KIND>
+__global__ void __launch_bounds__(SPLIT_BLOCK) split_exchange_kernel(
+    const K *keys, const void *vals_, uint64_t n, int shift0, const K *spl, int nsp, const uint32_t *tile_off,
+    const long long *delta, const unsigned long long *bounds, int nranks, K *const *dst_keys,
+    void *const *dst_vals) {
+  using V = typename ValT<VB>::T;
+  using S = ExchangeSmem<K, VB>;
+  constexpr int NW = SPLIT_BLOCK / 32;
+  extern __shared__ __align__(16) unsigned char xsm[];
+  K *stage = reinterpret_cast<K *>(xsm + S::keys_off);
+  V *vstage = reinterpret_cast<V *>(xsm + S::vals_off);
+  __shared__ uint32_t wrun[NW][16];
+  __shared__ uint32_t tb[17];
+  __shared__ uint32_t s_off[16];
+  __shared__ long long s_delta[16];
+  __shared__ unsigned long long s_bnd[9];
+  __shared__ K s_spl[16];
+  __shared__ K *s_dk[8];
+  __shared__ V *s_dv[8];
+  const KeyGeom<K, KIND> g{shift0};
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int ncls = 2 * nsp + 1;
+  if (tid < nsp) s_spl[tid] = spl[tid];
+  if (tid < 16) {
+    s_off[tid] = tile_off[size_t(blockIdx.x) * 16 + tid];
+    s_delta[tid] = tid < ncls ? delta[tid] : 0;
+    wrun[0][tid] = 0;
+  }
+  if (tid < NW * 16 && tid >= 16) (&wrun[0][0])[tid] = 0;
+  if (tid <= nranks) s_bnd[tid] = bounds[tid];
+  if (tid < nranks) {
+    s_dk[tid] = dst_keys[tid];
+    if constexpr (VB != 0) s_dv[tid] = static_cast<V *>(dst_vals[tid]);
+  }
+  __syncthreads();
+  const V *vals = static_cast<const V *>(vals_);
+  const uint64_t base = uint64_t(blockIdx.x) * SPLIT_TILE;
+  const int cnt = int(min64(SPLIT_TILE, n - base));
+  const int wbase = w * 32 * SPLIT_KPT;
+  const uint32_t lt = lanemask_lt();
+  K x[SPLIT_KPT];
+  V v[SPLIT_KPT];
+  uint32_t dr[SPLIT_KPT];  // class | rank-in-warp << 8
+#pragma unroll
+  for (int j = 0; j < SPLIT_KPT; ++j) {
+    const int e = wbase + 32 * j + lane;
+    const bool valid = e < cnt;
+    uint32_t d = 0xFFu;
+    if (valid) {
+      x[j] = keys[base + e];
+      if constexpr (VB != 0) v[j] = vals[base + e];
+      d = split_class(g.norm(x[j]), s_spl, nsp);
+    }
+    // stable rank among this warp's elements of the same class (element order j-major, lane-minor)
+    const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
+    const uint32_t below = __popc(peers & lt);
+    uint32_t old = 0;
+    if (valid && below == 0) {
+      old = wrun[w][d];
+      wrun[w][d] = old + __popc(peers);
+    }
+    old = __shfl_sync(0xFFFFFFFFu, old, __ffs(peers) - 1);
+    dr[j] = d | ((old + below) << 8);
+    __syncwarp();
+  }
+  __syncthreads();
+  if (tid < 16) {  // per-warp exclusive prefixes per class, then tile class bases
+    uint32_t run = 0;
+    for (int i = 0; i < NW; ++i) {
+      const uint32_t c = wrun[i][tid];
+      wrun[i][tid] = run;
+      run += c;
+    }
+    tb[tid + 1] = run;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    tb[0] = 0;
+    for (int c = 1; c <= 16; ++c) tb[c] += tb[c - 1];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < SPLIT_KPT; ++j) {
+    const int e = wbase + 32 * j + lane;
+    if (e < cnt) {
+      const uint32_t d = dr[j] & 0xFFu;
+      const uint32_t p = tb[d] + wrun[w][d] + (dr[j] >> 8);
+      stage[p] = x[j];
+      if constexpr (VB != 0) vstage[p] = v[j];
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < cnt; i += SPLIT_BLOCK) {
+    int c = 0;
+#pragma unroll
+    for (int k = 1; k < 16; ++k) c += (uint32_t(i) >= tb[k]) ? 1 : 0;
+    const uint64_t gpos = uint64_t(int64_t(s_off[c] + (uint32_t(i) - tb[c])) + s_delta[c]);
+    int d = 0;
+    for (int k = 1; k < nranks; ++k) d += (gpos >= s_bnd[k]) ? 1 : 0;
+    const uint64_t o = gpos - s_bnd[d];
+    s_dk[d][o] = stage[i];
+    if constexpr (VB != 0) s_dv[d][o] = vstage[i];
+  }
+  // the stores must be visible to the receiving GPUs once this grid is done
+  __threadfence_system();
 }
 
 }  // namespace bs

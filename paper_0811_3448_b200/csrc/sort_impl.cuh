@@ -122,6 +122,7 @@ struct Ws {
   int shift0;          // W - width_eff
   int kbits;           // W
   int stable;          // key-value sort: tiles use the look-back scan
+  uint32_t root_parity;  // buffer holding the input: 0 caller's, 1 the copy (bs_sort_from: the source)
 };
 
 
@@ -138,7 +139,7 @@ __global__ void init_kernel(Ws ws) {
   const KeyGeom<K, KIND> g{ws.shift0};
   if (n <= ws.local_max) {
     if (blockIdx.x == 0 && tid == 0) {
-      ws.tasks[0] = Task{0, uint32_t(n), 0};
+      ws.tasks[0] = Task{0, uint32_t(n), ws.root_parity};
       ws.ctl->ntasks = 1;
     }
     return;
@@ -153,7 +154,7 @@ __global__ void init_kernel(Ws ws) {
   __shared__ uint64_t s_or[32], s_and[32];
   // 4096-element strided sample of the encoded normalised key
   K o = 0, a = ~K(0);
-  const K *keys = static_cast<const K *>(ws.keys[0]);
+  const K *keys = static_cast<const K *>(ws.keys[ws.root_parity]);
   for (int i = tid; i < 4096; i += blockDim.x) {
     uint64_t idx = (uint64_t(2 * i + 1) * n) / 8192;
     K nk = g.norm(keys[idx]);
@@ -176,7 +177,7 @@ __global__ void init_kernel(Ws ws) {
     K var = oo ^ aa;
     int dig = var ? (KeyTraits<K>::clz(var) >> 3) : 0;
     if (dig >= ws.ndig) dig = 0;
-    ws.buckets[0][0] = Bucket{0, uint32_t(n), 0, uint32_t(dig), 0, ACT_SCATTER, 0};
+    ws.buckets[0][0] = Bucket{0, uint32_t(n), 0, uint32_t(dig), ws.root_parity, ACT_SCATTER, 0};
     ws.bor[0][0] = 0;
     ws.band[0][0] = ~uint64_t(0);
     ws.ctl->nbuckets[0] = 1;
@@ -329,44 +330,76 @@ __global__ void __launch_bounds__(BLOCK, 1) hist16_kernel(Ws ws) {
   // input, with no per-key overflow test.
   constexpr int GPE = 32768 / (BLOCK * EPG);  // granules per thread per epoch
   static_assert(GPE % UNR == 0 && GPE > 0, "whole batches per epoch");
-  auto count = [&](K x) {
-    const K nk = g.norm(x);
-    o |= nk;
-    a &= nk;
-    const uint32_t p = (uint32_t(nk >> shA) & msk) << post;
-    atomicAdd(&hw[p >> 1], 1u + (p & 1u) * 0xFFFFu);
-  };
-  auto granule = [&](uint64_t gi, const uint4 &v) {
-    K kk[EPG];
-    if constexpr (sizeof(K) == 4) {
-      kk[0] = K(v.x), kk[1] = K(v.y), kk[2 % EPG] = K(v.z), kk[3 % EPG] = K(v.w);
-    } else {
-      kk[0] = K((uint64_t(v.y) << 32) | v.x);
-      kk[1 % EPG] = K((uint64_t(v.w) << 32) | v.z);
-    }
-    const int64_t e0 = int64_t(gi * EPG) - int64_t(head);
-    if (e0 >= 0 && e0 + EPG <= int64_t(n)) {
-#pragma unroll
-      for (int j = 0; j < EPG; ++j) count(kk[j]);
-    } else {
-#pragma unroll
-      for (int j = 0; j < EPG; ++j)
-        if (e0 + j >= 0 && e0 + j < int64_t(n)) count(kk[j]);
-    }
-  };
+  // A batch = UNR granules per thread.  The batch's OR/AND masks (which the
+  // root's masks need anyway) show when all of a thread's keys share one bin;
+  // when all 32 lanes share the same bin (sorted or constant runs) one add of
+  // 32*UNR*EPG replaces that many same-address atomics.  The epoch bound is
+  // unchanged (the same keys are counted).
   for (uint64_t eb = g0; eb < g1; eb += uint64_t(GPE) * BLOCK) {  // block-uniform epochs
 #pragma unroll
     for (int u0 = 0; u0 < GPE; u0 += UNR) {
       uint4 v[UNR];
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        const uint64_t gi = eb + uint64_t(u0 + u) * BLOCK + tid;
+      for (int u = 0; u < UNR; ++u) {  // a warp's batch: 32*UNR consecutive granules
+        const uint64_t gi = eb + uint64_t(u0) * BLOCK + uint64_t(w) * (32 * UNR) + uint64_t(u) * 32 + lane;
         v[u] = gi < g1 ? __ldcs(gsrc + gi) : make_uint4(0, 0, 0, 0);
       }
+      K nk[UNR * EPG];
+      uint32_t valid = 0;
+      K ob = 0, ab = ~K(0);
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
-        const uint64_t gi = eb + uint64_t(u0 + u) * BLOCK + tid;
-        if (gi < g1) granule(gi, v[u]);
+        const uint64_t gi = eb + uint64_t(u0) * BLOCK + uint64_t(w) * (32 * UNR) + uint64_t(u) * 32 + lane;
+        K kk[EPG];
+        if constexpr (sizeof(K) == 4) {
+          kk[0] = K(v[u].x), kk[1] = K(v[u].y), kk[2 % EPG] = K(v[u].z), kk[3 % EPG] = K(v[u].w);
+        } else {
+          kk[0] = K((uint64_t(v[u].y) << 32) | v[u].x);
+          kk[1 % EPG] = K((uint64_t(v[u].w) << 32) | v[u].z);
+        }
+        const int64_t e0 = int64_t(gi * EPG) - int64_t(head);
+        if (gi < g1 && e0 >= 0 && e0 + EPG <= int64_t(n)) {
+          valid |= ((1u << EPG) - 1u) << (u * EPG);
+#pragma unroll
+          for (int j = 0; j < EPG; ++j) {
+            nk[u * EPG + j] = g.norm(kk[j]);
+            ob |= nk[u * EPG + j];
+            ab &= nk[u * EPG + j];
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < EPG; ++j) {
+            nk[u * EPG + j] = g.norm(kk[j]);
+            if (gi < g1 && e0 + j >= 0 && e0 + j < int64_t(n)) {
+              valid |= 1u << (u * EPG + j);
+              ob |= nk[u * EPG + j];
+              ab &= nk[u * EPG + j];
+            }
+          }
+        }
+      }
+      o |= ob;
+      a &= ab;
+      constexpr uint32_t ALL = (1u << (UNR * EPG)) - 1u;
+      const uint32_t pb = (uint32_t(ob >> shA) & msk) << post;
+      const bool same = valid == ALL && ((uint32_t((ob ^ ab) >> shA) & msk) == 0u);
+      const uint32_t lead = __shfl_sync(0xFFFFFFFFu, pb, 0);
+      if (__all_sync(0xFFFFFFFFu, same && pb == lead)) {
+        if (lane == 0) atomicAdd(&hw[lead >> 1], (32u * UNR * EPG) << (16u * (lead & 1u)));
+      } else if (valid == ALL) {
+#pragma unroll
+        for (int i = 0; i < UNR * EPG; ++i) {
+          const uint32_t p = (uint32_t(nk[i] >> shA) & msk) << post;
+          atomicAdd(&hw[p >> 1], 1u + (p & 1u) * 0xFFFFu);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < UNR * EPG; ++i) {
+          if ((valid >> i) & 1u) {
+            const uint32_t p = (uint32_t(nk[i] >> shA) & msk) << post;
+            atomicAdd(&hw[p >> 1], 1u + (p & 1u) * 0xFFFFu);
+          }
+        }
       }
     }
     __syncthreads();
@@ -1592,6 +1625,88 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
           done = true;
         }
         // else: too many repeats for the overflow list -> LSD passes below
+      }
+      // Bin sort (keys only, any span): one counting pass on the top B varying
+      // bits with 2^B >= n bins (about one key per bin), then every key finds
+      // its place inside its bin by comparing itself with the bin's few other
+      // keys -- one shared atomic, two scattered stores and ~2 loads per key
+      // instead of one ranking pass per varying digit.  A task with a bin of
+      // more than BIN_MAX keys (heavy duplicates) takes the LSD passes below.
+      if (!done && n >= 64) {
+        constexpr int BIN_LOG_MAX = 13;  // 8192 counters fit the bitmap region
+        static_assert(sizeof(uint32_t) * (1u << BIN_LOG_MAX) <= S::bm_bytes, "bins fit");
+        const int hb = W - 1 - KeyTraits<K>::clz(var);  // top varying bit of the normalised key
+        int B = 32 - __clz(uint32_t(n - 1));
+        B = min(min(B, BIN_LOG_MAX), hb + 1);
+        const int sh = hb + 1 - B;
+        const uint32_t nbins = 1u << B, bmask = nbins - 1u;
+        uint32_t *bins = whist_all;
+        for (uint32_t i = tid; i < nbins; i += BLOCK) bins[i] = 0;
+        __syncthreads();
+        Ranks<KPT> slot;  // arrival slot inside the bin
+        slot.clear();
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+          if (j >= kk) break;
+          if (32 * j + lane < nvw) slot.set(j, atomicAdd(&bins[uint32_t(g.norm(x[j]) >> sh) & bmask], 1u));
+        }
+        __syncthreads();
+        const uint32_t bpt = (nbins + BLOCK - 1) / BLOCK;
+        const uint32_t q0 = min(nbins, uint32_t(tid) * bpt), q1 = min(nbins, q0 + bpt);
+        if (tid == 0) misc[48] = 0;
+        uint32_t c = 0, c2 = 0;
+        for (uint32_t q = q0; q < q1; ++q) {
+          const uint32_t v = bins[q];
+          c += v;
+          c2 += v * v;
+        }
+        __syncthreads();
+        c2 = __reduce_add_sync(0xFFFFFFFFu, c2);
+        if (lane == 0 && c2) atomicAdd(&misc[48], c2);
+        __syncthreads();
+        if (misc[48] <= 8u * uint32_t(n)) {
+          uint32_t run = block_scan_excl<BLOCK>(c, misc);
+          for (uint32_t q = q0; q < q1; ++q) {
+            const uint32_t v = bins[q];
+            bins[q] = run;
+            run += v;
+          }
+          __syncthreads();
+          // bin order (arbitrary inside a bin)
+#pragma unroll
+          for (int j = 0; j < KPT; ++j) {
+            if (j >= kk) break;
+            if (32 * j + lane < nvw) kb[bins[uint32_t(g.norm(x[j]) >> sh) & bmask] + slot.get(j)] = x[j];
+          }
+          __syncthreads();
+          // place inside the bin: smaller keys, then equal keys that arrived earlier
+          Ranks<KPT> fin;
+          fin.clear();
+#pragma unroll
+          for (int j = 0; j < KPT; ++j) {
+            if (j >= kk) break;
+            if (32 * j + lane < nvw) {
+              const K nk = g.norm(x[j]);
+              const uint32_t d = uint32_t(nk >> sh) & bmask;
+              const uint32_t s = bins[d], e = d < bmask ? bins[d + 1] : uint32_t(n);
+              const uint32_t p = s + slot.get(j);
+              uint32_t r = 0;
+              for (uint32_t i = s; i < e; ++i) {
+                const K y = g.norm(kb[i]);
+                r += (y < nk || (y == nk && i < p)) ? 1u : 0u;
+              }
+              fin.set(j, s + r);
+            }
+          }
+          __syncthreads();
+#pragma unroll
+          for (int j = 0; j < KPT; ++j) {
+            if (j >= kk) break;
+            if (32 * j + lane < nvw) kb[fin.get(j)] = x[j];
+          }
+          __syncthreads();
+          done = true;
+        }
       }
     }
     if (!done) {

@@ -18,12 +18,19 @@ sketches (``PAPER.md:479``) and SURVEY §8e specifies:
    (rank, local index) order, so destination loads stay balanced even when
    one key value holds a large share of the data, and a stable sort stays
    stable across ranks.
-4. **Data exchange** -- ``all_to_all_single`` (NCCL over NVLink/NVSwitch on
-   B200; gloo in the CPU tests); every destination's data is one contiguous
-   run of the partitioned shard.
-5. **Local sort** -- the received runs arrive in source-rank order and are
-   sorted by the single-GPU ``bs_sort`` (stable), so rank r ends up owning the
-   r-th contiguous slice of the global sorted order.
+4. **Data exchange** -- the product path (``exchange="peer"``) fuses steps 2
+   and 4: once every rank's class counts are known, every element's position
+   in the global class-major order is too, so ``bs_split_exchange`` stores
+   each element straight into its destination rank's receive buffer over
+   NVLink / NVSwitch peer memory (buffers mapped once with CUDA IPC and
+   reused), one kernel instead of partition -> send buffer -> all-to-all-v.
+   ``exchange="collective"`` keeps the partition + ``all_to_all_single``
+   (NCCL) form as the baseline and for the CPU (gloo) tests.
+5. **Local sort** -- each receive buffer holds its global positions
+   [B[d], B[d+1]) in class-major, source-rank order and is sorted by the
+   single-GPU sort (stable; ``bs_sort_from`` writes the result to a fresh
+   tensor, the receive buffer is its ping-pong copy), so rank r ends up owning
+   the r-th contiguous slice of the global sorted order.
 
 The per-rank device steps go through a ``LocalOps`` object; the product uses
 :class:`CudaOps` (the C ABI).  The host logic (splitters, tie division,
@@ -38,7 +45,8 @@ import numpy as np
 
 from . import _lib, device
 
-__all__ = ["CudaOps", "DistResult", "choose_splitters", "boundaries", "send_counts", "dist_sort"]
+__all__ = ["CudaOps", "DistResult", "PeerBuffers", "choose_splitters", "boundaries", "send_counts",
+           "exchange_plan", "dist_sort"]
 
 
 @dataclass
@@ -98,6 +106,145 @@ class CudaOps:
         if keys.numel() > 1:
             device.sort_words_device(keys, values, width=self.width, key_kind=self.key_kind)
         return keys, values
+
+    # ---- fused peer exchange (exchange="peer") ----
+    def split_count(self, keys, splitters, nranks: int):
+        """Class counts of this shard (device uint64 as int64); tile offsets stay in self._split_ws."""
+        t = device.require_cuda()
+        L = _lib.lib()
+        n = keys.numel()
+        kb = keys.element_size()
+        counts = t.zeros(2 * nranks - 1, dtype=t.int64, device=keys.device)
+        need = L.bs_split_workspace_bytes(n, kb, 0, nranks)
+        ws = getattr(self, "_split_ws", None)
+        if ws is None or ws.numel() < need or ws.device != keys.device:
+            ws = self._split_ws = t.empty(need, dtype=t.uint8, device=keys.device)
+        with t.cuda.device(keys.device):
+            rc = L.bs_split_count(keys.data_ptr(), n, kb, self.width, self.key_kind, splitters.data_ptr(), nranks,
+                                  counts.data_ptr(), ws.data_ptr(), ws.numel(), device.stream_ptr(keys.device))
+        _lib.check(rc)
+        return counts
+
+    def exchange(self, keys, values, splitters, nranks: int, delta: np.ndarray, bounds: np.ndarray, bufs):
+        """Store every element into its destination's receive buffer (bs_split_exchange)."""
+        t = device.require_cuda()
+        L = _lib.lib()
+        dev = keys.device
+        d_delta = t.from_numpy(np.ascontiguousarray(delta, dtype=np.int64)).to(dev, non_blocking=True)
+        d_bounds = t.from_numpy(np.ascontiguousarray(bounds, dtype=np.int64)).to(dev, non_blocking=True)
+        ws = self._split_ws
+        with t.cuda.device(dev):
+            rc = L.bs_split_exchange(keys.data_ptr(), values.data_ptr() if values is not None else None,
+                                     keys.numel(), keys.element_size(),
+                                     values.element_size() if values is not None else 0, self.width,
+                                     self.key_kind, splitters.data_ptr(), nranks, d_delta.data_ptr(),
+                                     d_bounds.data_ptr(), bufs.key_table.data_ptr(),
+                                     bufs.val_table.data_ptr() if values is not None else None,
+                                     ws.data_ptr(), ws.numel(), device.stream_ptr(dev))
+        _lib.check(rc)
+
+    def sort_from(self, bufs, count: int, key_dtype, val_dtype):
+        """Sort this rank's receive buffer into fresh tensors (bs_sort_from)."""
+        t = device.require_cuda()
+        L = _lib.lib()
+        dev = bufs.device
+        out_k = t.empty(count, dtype=key_dtype, device=dev)
+        out_v = t.empty(count, dtype=val_dtype, device=dev) if val_dtype is not None else None
+        kb = out_k.element_size()
+        vb = out_v.element_size() if out_v is not None else 0
+        ws = device.workspaces.get(L.bs_sort_from_workspace_bytes(count, kb, vb), dev)
+        with t.cuda.device(dev):
+            rc = L.bs_sort_from(bufs.local_keys, bufs.local_vals if vb else None, out_k.data_ptr(),
+                                out_v.data_ptr() if out_v is not None else None, count, kb, vb, self.width, 0,
+                                self.key_kind, ws.data_ptr(), ws.numel(), device.stream_ptr(dev))
+        _lib.check(rc)
+        return out_k, out_v
+
+
+class PeerBuffers:
+    """Per-rank receive buffers mapped into every rank's address space (CUDA IPC).
+
+    One allocation per rank holds ``cap`` keys (and ``cap`` values); the
+    handles are all-gathered once and every peer's buffer is opened, so the
+    exchange kernel can store to ``key_table[d]`` for any destination d.  The
+    buffers are reused across calls and regrown collectively (every rank
+    derives the same required capacity from the all-gathered class counts).
+    """
+
+    def __init__(self, group, dev):
+        self.group = group
+        self.device = dev
+        self.cap = 0
+        self.kb = self.vb = 0
+        self._local = None
+        self._peers = []
+        self.key_table = self.val_table = None
+        self.local_keys = self.local_vals = None
+
+    def ensure(self, cap: int, kb: int, vb: int) -> "PeerBuffers":
+        import ctypes
+
+        import torch
+
+        if cap <= self.cap and kb == self.kb and vb == self.vb:
+            return self
+        self.close()
+        L = _lib.lib()
+        cap = max(1024, int(cap * 1.125) + 1024)
+        voff = (cap * kb + 255) // 256 * 256
+        nbytes = voff + cap * vb
+        R = _world(self.group)
+        me = _rank(self.group)
+        hb = int(L.bs_ipc_handle_bytes())
+        handle = (ctypes.c_ubyte * hb)()
+        ptr = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(L.bs_ipc_alloc(nbytes, ctypes.byref(ptr), handle))
+        self._local = ptr.value
+        handles = _all_gather_np(np.frombuffer(bytes(handle), dtype=np.uint8), self.group, self.device)
+        bases = []
+        with torch.cuda.device(self.device):
+            for r in range(R):
+                if r == me:
+                    bases.append(self._local)
+                    continue
+                p = ctypes.c_void_p()
+                _lib.check(L.bs_ipc_open(handles[r].tobytes(), ctypes.byref(p)))
+                self._peers.append(p.value)
+                bases.append(p.value)
+        self.key_table = torch.tensor(bases, dtype=torch.int64, device=self.device)
+        self.val_table = torch.tensor([b + voff for b in bases], dtype=torch.int64, device=self.device)
+        self.local_keys = self._local
+        self.local_vals = self._local + voff
+        self.cap, self.kb, self.vb = cap, kb, vb
+        return self
+
+    def close(self) -> None:
+        if self._local is None:
+            return
+        import torch
+
+        L = _lib.lib()
+        torch.cuda.synchronize(self.device)
+        _barrier(self.group, self.device)  # nobody still stores into or reads from these buffers
+        for p in self._peers:
+            L.bs_ipc_close(p)
+        _barrier(self.group, self.device)  # every peer mapping of our buffer is gone
+        L.bs_ipc_free(self._local)
+        self._local = None
+        self._peers = []
+        self.cap = 0
+
+
+_PEER_BUFFERS: dict = {}
+
+
+def _peer_buffers(group, dev) -> PeerBuffers:
+    key = (id(group), str(dev))
+    b = _PEER_BUFFERS.get(key)
+    if b is None:
+        b = _PEER_BUFFERS[key] = PeerBuffers(group, dev)
+    return b
 
 
 def choose_splitters(sorted_samples: np.ndarray, nranks: int) -> np.ndarray:
@@ -163,18 +310,85 @@ def send_counts(class_counts: np.ndarray, B: np.ndarray, rank: int) -> list[int]
     return out
 
 
+def exchange_plan(class_counts: np.ndarray, nranks: int, rank: int):
+    """Host side of the fused exchange for source ``rank``.
+
+    Returns (bounds B[0..R], delta[2R-1], recv_counts[R]): destination d owns
+    global class-major positions [B[d], B[d+1]); this rank's shard-local
+    class-major position p of a class-c element maps to the global position
+    p + delta[c] (global order: class, then source rank, then shard index --
+    the order ``send_counts`` / the all-to-all path produce).
+    """
+    cc = np.asarray(class_counts, dtype=np.int64)
+    B = boundaries(cc, nranks)
+    totals = cc.sum(axis=0)
+    cstart = np.concatenate([[0], np.cumsum(totals)])[:-1]
+    gbase = cstart + cc[:rank].sum(axis=0)
+    lbase = np.concatenate([[0], np.cumsum(cc[rank])])[:-1]
+    return B, (gbase - lbase).astype(np.int64), np.diff(B).astype(np.int64)
+
+
+def _world(group) -> int:
+    import torch.distributed as dist
+
+    return dist.get_world_size(group) if dist.is_initialized() else 1
+
+
+def _rank(group) -> int:
+    import torch.distributed as dist
+
+    return dist.get_rank(group) if dist.is_initialized() else 0
+
+
+def _on_device(group) -> bool:
+    import torch.distributed as dist
+
+    return dist.get_backend(group) == "nccl"
+
+
+def _all_gather_np(a: np.ndarray, group, dev) -> np.ndarray:
+    """All-gather a small host array over ``group`` -> [R, *a.shape] (device tensors for NCCL)."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.from_numpy(np.ascontiguousarray(a).copy())
+    if _on_device(group):
+        t = t.to(dev)
+    out = [torch.empty_like(t) for _ in range(_world(group))]
+    dist.all_gather(out, t, group=group)
+    return np.stack([o.cpu().numpy() for o in out])
+
+
+def _barrier(group, dev) -> None:
+    """Order every rank's queued device work before what follows on any rank."""
+    import torch
+    import torch.distributed as dist
+
+    if _on_device(group):  # stream-ordered: a one-element all-reduce on the current stream
+        dist.all_reduce(torch.zeros(1, device=dev), group=group)
+    else:
+        torch.cuda.synchronize(dev)
+        dist.barrier(group=group)
+
+
 def dist_sort(keys, values=None, *, width: int, key_kind: int = _lib.BS_KEY_UNSIGNED, ops=None, group=None,
-              samples_per_rank: int = 4096) -> DistResult:
+              samples_per_rank: int = 4096, exchange: str = "auto") -> DistResult:
     """Globally sort the shards held by all ranks of ``group``.
 
     ``keys`` (and ``values``) are this rank's contiguous 1-D tensors (CUDA for
     the product path).  Returns this rank's slice of the global order; the
-    concatenation over ranks 0..R-1 is the sorted whole.
+    concatenation over ranks 0..R-1 is the sorted whole.  ``exchange``:
+    "peer" (fused partition + peer-memory stores, the product path for CUDA
+    tensors), "collective" (partition + all-to-all-v), or "auto".
     """
     import torch
     import torch.distributed as dist
 
     ops = ops or CudaOps(width, key_kind)
+    if exchange == "auto":
+        exchange = "peer" if isinstance(ops, CudaOps) and getattr(keys, "is_cuda", False) else "collective"
+    if exchange not in ("peer", "collective"):
+        raise ValueError(f"unknown exchange {exchange!r}")
     R = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     if R == 1:
@@ -195,6 +409,23 @@ def dist_sort(keys, values=None, *, width: int, key_kind: int = _lib.BS_KEY_UNSI
     ssorted = ops.sort_samples(allsmp)
     spl_host = choose_splitters(_to_unsigned_np(ssorted), R)
     splitters = torch.from_numpy(spl_host.view(_np_signed(keys.element_size()))).to(dev)
+    if exchange == "peer":
+        # 2+3. class counts of every shard (the host read also orders this
+        # rank's previous local sort -- which reads its receive buffer --
+        # before the all-gather, so no peer overwrites a buffer still in use)
+        cc = _all_gather_np(ops.split_count(keys, splitters, R).cpu().numpy(), group, dev).astype(np.int64)
+        B, delta, rcounts = exchange_plan(cc, R, rank)
+        kb = keys.element_size()
+        vb = values.element_size() if values is not None else 0
+        bufs = _peer_buffers(group, dev).ensure(int(rcounts.max()), kb, vb)
+        # 4. fused partition + peer stores, then every rank's stores land
+        ops.exchange(keys, values, splitters, R, delta, B, bufs)
+        _barrier(group, dev)
+        # 5. local sort out of the receive buffer
+        out_k, out_v = ops.sort_from(bufs, int(rcounts[rank]), keys.dtype,
+                                     values.dtype if values is not None else None)
+        scounts = send_counts(cc, B, rank)
+        return DistResult(out_k, out_v, scounts, [send_counts(cc, B, src)[rank] for src in range(R)])
     # 2. destination partition
     send_k, send_v, class_counts = ops.split(keys, values, splitters, R)
     # 3. count exchange + tie division

@@ -160,7 +160,31 @@ DISTS = {
     "dense_dups_sparse_u32": lambda n: _top_low(7, n, 1 << 10, 1 << 13),
     # ~16K-key tasks for the big dense variant, with a few repeats
     "big_dense_u32": lambda n: _top_low(8, n, 1 << 8, 1 << 16),
+    # local bin sort: equal keys ranked inside a bin (each value 2 / 3 times) and
+    # the comparison-budget fallback to LSD (each value 41 times)
+    "dup2_u64": lambda n: _repeated(9, n, 2),
+    "dup3_u32": lambda n: _repeated(12, n, 3).astype(np.uint32),
+    "dup41_u64": lambda n: _repeated(10, n, 41),
+    # sorted runs in random order (hist16 warp-aggregated bins for some warps only)
+    "sorted_runs_u32": lambda n: _sorted_runs(11, n, 1000),
 }
+
+
+def _repeated(seed, n, k):
+    """u64 keys: random values, each repeated k times, shuffled."""
+    r = np.random.default_rng(seed)
+    v = r.integers(0, 1 << 63, (n + k - 1) // k, dtype=np.uint64) * np.uint64(2)
+    x = np.repeat(v, k)[:n]
+    r.shuffle(x)
+    return x
+
+
+def _sorted_runs(seed, n, run):
+    r = np.random.default_rng(seed)
+    x = np.sort(r.integers(0, 1 << 32, n, dtype=np.uint64).astype(np.uint32))
+    blocks = [x[i:i + run] for i in range(0, n, run)]
+    order = r.permutation(len(blocks))
+    return np.concatenate([blocks[i] for i in order])
 
 
 def _top_low(seed, n, ntop, nlow):
@@ -395,6 +419,25 @@ def test_hist16_spills_exact(cuda, kv):
         got = x.copy()
         bs.sort(got, UnsignedCodec(32), with_metrics=False)
         assert np.array_equal(got, np.sort(x))
+
+
+@pytest.mark.parametrize("head", [0, 1, 3])
+def test_sorted_input_unaligned_views(cuda, head):
+    # already-sorted / reverse-sorted device views starting off a 16-byte boundary:
+    # hist16's warp-uniform bin adds must count ragged head and tail granules exactly
+    import torch
+
+    from paper_0811_3448_b200 import device
+
+    n = (1 << 22) + 5
+    base = np.sort(np.random.default_rng(23).integers(0, 1 << 32, n + head, dtype=np.uint64).astype(np.uint32))
+    for x in (base, base[::-1].copy()):
+        t = torch.from_numpy(x.view(np.int32)).cuda()
+        v = t[head:]
+        device.sort_words_device(v, width=32)
+        got = v.cpu().numpy().view(np.uint32)
+        assert np.array_equal(got, np.sort(x[head:]))
+        assert np.array_equal(t[:head].cpu().numpy().view(np.uint32), x[:head])
 
 
 def test_hist16_constant_second_digit(cuda):
