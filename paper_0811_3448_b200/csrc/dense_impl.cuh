@@ -12,7 +12,7 @@
 //               its bit in the presence bitmap B1 with one shared atomicOr.
 //               A key that finds its bit set is a repeat: the second copy sets
 //               B2, the third B3, later ones go to a small overflow list; a
-//               repeat also marks its word in the summary bitmaps RF / OF.
+//               an overflow entry also marks its word in the summary bitmap OF.
 //               The input slot is released to the producer warp right here.
 //   count/scan: thread t owns bitmap words 4t..4t+3 (one uint4 of B1):
 //               popc(B1) [+ popc(B2) + popc(B3) + listed overflow copies for
@@ -56,8 +56,7 @@ struct DenseSmem {
   static constexpr size_t b1_off = stg_off + kbuf + 16;
   static constexpr size_t b2_off = b1_off + sizeof(uint32_t) * NW;
   static constexpr size_t b3_off = b2_off + sizeof(uint32_t) * NW;
-  static constexpr size_t rf_off = b3_off + sizeof(uint32_t) * NW;  // word has repeats
-  static constexpr size_t of_off = rf_off + sizeof(uint32_t) * NS;  // word has overflow entries
+  static constexpr size_t of_off = b3_off + sizeof(uint32_t) * NW;  // word has overflow entries
   static constexpr size_t dup_off = of_off + sizeof(uint32_t) * NS;
   static constexpr size_t misc_off = dup_off + sizeof(uint32_t) * DUPCAP;
   static constexpr size_t bars_off = misc_off + sizeof(uint32_t) * 64;
@@ -74,7 +73,6 @@ __global__ void __launch_bounds__(BLOCK + 32, BIG ? 1 : 2) dense_kernel(Ws ws, i
   uint32_t *B1 = reinterpret_cast<uint32_t *>(smem + S::b1_off);
   uint32_t *B2 = reinterpret_cast<uint32_t *>(smem + S::b2_off);
   uint32_t *B3 = reinterpret_cast<uint32_t *>(smem + S::b3_off);
-  uint32_t *RF = reinterpret_cast<uint32_t *>(smem + S::rf_off);
   uint32_t *OF = reinterpret_cast<uint32_t *>(smem + S::of_off);
   uint32_t *dup = reinterpret_cast<uint32_t *>(smem + S::dup_off);
   uint32_t *misc = reinterpret_cast<uint32_t *>(smem + S::misc_off);
@@ -140,13 +138,14 @@ __global__ void __launch_bounds__(BLOCK + 32, BIG ? 1 : 2) dense_kernel(Ws ws, i
   constexpr int NWARP = BLOCK / 32;
   constexpr int EPG = 16 / int(sizeof(K));  // keys per 16-byte granule
   constexpr int NDUP = 32;                  // misc[NDUP]: overflow count
+  constexpr int GPT = (CAP / EPG + 2 + BLOCK - 1) / BLOCK;  // granules per thread (incl. head shift)
   // every bitmap starts clear; afterwards owners clear what they used
   for (int q = tid; q < S::NW / 4; q += BLOCK) {
     reinterpret_cast<uint4 *>(B1)[q] = make_uint4(0, 0, 0, 0);
     reinterpret_cast<uint4 *>(B2)[q] = make_uint4(0, 0, 0, 0);
     reinterpret_cast<uint4 *>(B3)[q] = make_uint4(0, 0, 0, 0);
   }
-  if (tid < S::NS) RF[tid] = OF[tid] = 0;
+  if (tid < S::NS) OF[tid] = 0;
   if (tid == 0) misc[NDUP] = 0;
   named_sync<BLOCK>();
   const KeyGeom<K, KIND> g{0};
@@ -160,24 +159,23 @@ __global__ void __launch_bounds__(BLOCK + 32, BIG ? 1 : 2) dense_kernel(Ws ws, i
     const uint32_t vmask = (span >= 32) ? 0xFFFFFFFFu : ((1u << span) - 1u);
     const K common = K((uint64_t(f.tile0) << 32) | f.headv);
     // ---- insert: one presence atomic per key, 16-byte granules ----
+    const K *slot = reinterpret_cast<const K *>(smem + S::dbuf_off + s * S::kbuf);
+    const int head = int(f.headk);
+    const int ngr = (head + n + EPG - 1) / EPG;
     {
-      const K *slot = reinterpret_cast<const K *>(smem + S::dbuf_off + s * S::kbuf);
-      const int head = int(f.headk);
-      const int ngr = (head + n + EPG - 1) / EPG;
-      // repeats (rare for dense tasks): second copy -> B2, third -> B3, later
-      // ones -> overflow list
-      auto repeat = [&](uint32_t idx) {
+      // third and later copies (rare): B3, then the overflow list
+      auto third_copy = [&](uint32_t idx) {
         const uint32_t q = idx >> 5, bit = 1u << (idx & 31u);
-        const uint32_t o2 = atomicOr(&B2[q], bit);
-        if (!(o2 & bit)) {
-          if (!o2) atomicOr(&RF[q >> 5], 1u << (q & 31u));
-        } else if (atomicOr(&B3[q], bit) & bit) {
+        if (atomicOr(&B3[q], bit) & bit) {
           const uint32_t sl = atomicAdd(&misc[NDUP], 1u);
           if (sl < uint32_t(S::DUPCAP)) dup[sl] = idx;
           atomicOr(&OF[q >> 5], 1u << (q & 31u));
         }
       };
-      for (int gi = tid; gi < ngr; gi += BLOCK) {
+#pragma unroll
+      for (int u = 0; u < GPT; ++u) {
+        const int gi = tid + u * BLOCK;
+        if (gi >= ngr) break;
         const uint4 v = reinterpret_cast<const uint4 *>(slot)[gi];
         K kk[EPG];
         if constexpr (sizeof(K) == 4) {
@@ -196,10 +194,19 @@ __global__ void __launch_bounds__(BLOCK + 32, BIG ? 1 : 2) dense_kernel(Ws ws, i
           const uint32_t bit = ok ? (1u << (idx[j] & 31u)) : 0u;
           if (atomicOr(&B1[idx[j] >> 5], bit) & bit) rep |= 1u << j;
         }
-        if (rep) {
+        // second copies: ~3% of the keys, so nearly every warp has some --
+        // predicated atomics, no divergent branch
+        uint32_t third = 0;
+#pragma unroll
+        for (int j = 0; j < EPG; ++j) {
+          const uint32_t bit = ((rep >> j) & 1u) << (idx[j] & 31u);
+          if (rep & (1u << j))
+            if (atomicOr(&B2[idx[j] >> 5], bit) & bit) third |= 1u << j;
+        }
+        if (third) {
 #pragma unroll
           for (int j = 0; j < EPG; ++j)
-            if ((rep >> j) & 1u) repeat(idx[j]);
+            if ((third >> j) & 1u) third_copy(idx[j]);
         }
       }
     }
@@ -219,7 +226,7 @@ __global__ void __launch_bounds__(BLOCK + 32, BIG ? 1 : 2) dense_kernel(Ws ws, i
         reinterpret_cast<uint4 *>(B2)[q] = make_uint4(0, 0, 0, 0);
         reinterpret_cast<uint4 *>(B3)[q] = make_uint4(0, 0, 0, 0);
       }
-      if (tid < S::NS) RF[tid] = OF[tid] = 0;
+      if (tid < S::NS) OF[tid] = 0;
       if (tid == 0) misc[NDUP] = 0;
       named_sync<BLOCK>();
       continue;
@@ -228,22 +235,27 @@ __global__ void __launch_bounds__(BLOCK + 32, BIG ? 1 : 2) dense_kernel(Ws ws, i
     const int nw = span <= 7 ? 4 : (1 << (span - 5));
     const bool own = 4 * tid < nw;
     uint4 b1 = make_uint4(0, 0, 0, 0);
-    uint32_t rf = 0, of = 0;  // 4-bit masks of this thread's marked words
+    uint32_t of = 0;  // 4-bit mask of this thread's words with overflow entries
+    uint4 b2 = make_uint4(0, 0, 0, 0), b3 = make_uint4(0, 0, 0, 0);
     if (own) {
       b1 = reinterpret_cast<const uint4 *>(B1)[tid];
-      rf = (RF[tid >> 3] >> (4 * (tid & 7))) & 0xFu;
-      of = (OF[tid >> 3] >> (4 * (tid & 7))) & 0xFu;
-    }
-    uint32_t c = __popc(b1.x) + __popc(b1.y) + __popc(b1.z) + __popc(b1.w);
-    uint4 b2 = make_uint4(0, 0, 0, 0), b3 = make_uint4(0, 0, 0, 0);
-    if (rf) {
       b2 = reinterpret_cast<const uint4 *>(B2)[tid];
       b3 = reinterpret_cast<const uint4 *>(B3)[tid];
-      c += __popc(b2.x) + __popc(b2.y) + __popc(b2.z) + __popc(b2.w);
-      c += __popc(b3.x) + __popc(b3.y) + __popc(b3.z) + __popc(b3.w);
-      if (of)
-        for (uint32_t t = 0; t < ndup; ++t) c += ((dup[t] >> 7) == uint32_t(tid)) ? 1u : 0u;
+      of = (OF[tid >> 3] >> (4 * (tid & 7))) & 0xFu;
     }
+    uint32_t cw[4] = {uint32_t(__popc(b1.x) + __popc(b2.x) + __popc(b3.x)),
+                      uint32_t(__popc(b1.y) + __popc(b2.y) + __popc(b3.y)),
+                      uint32_t(__popc(b1.z) + __popc(b2.z) + __popc(b3.z)),
+                      uint32_t(__popc(b1.w) + __popc(b2.w) + __popc(b3.w))};
+    if (of)
+      for (uint32_t t = 0; t < ndup; ++t) {
+        const uint32_t q = dup[t] >> 5;
+        if ((q >> 2) == uint32_t(tid)) {
+          const uint32_t jj = q & 3u;
+          cw[0] += jj == 0u, cw[1] += jj == 1u, cw[2] += jj == 2u, cw[3] += jj == 3u;
+        }
+      }
+    const uint32_t c = cw[0] + cw[1] + cw[2] + cw[3];
     uint32_t incl = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -264,7 +276,7 @@ __global__ void __launch_bounds__(BLOCK + 32, BIG ? 1 : 2) dense_kernel(Ws ws, i
     }
     const uint32_t pos = __shfl_sync(0xFFFFFFFFu, wi - wt, w) + incl - c;
     // summary words are read (above) before S2; clear them for the next task
-    if (tid < S::NS) RF[tid] = OF[tid] = 0;
+    if (tid < S::NS) OF[tid] = 0;
     if (tid == 0) misc[NDUP] = 0;
     // ---- enumerate into the staging buffer (shifted to the output's 16-byte phase) ----
     K *dst = static_cast<K *>(ws.keys[0]) + f.start;
@@ -327,10 +339,8 @@ __global__ void __launch_bounds__(BLOCK + 32, BIG ? 1 : 2) dense_kernel(Ws ws, i
         }
       }
       if (b1.x | b1.y | b1.z | b1.w) reinterpret_cast<uint4 *>(B1)[tid] = make_uint4(0, 0, 0, 0);
-      if (rf) {
-        reinterpret_cast<uint4 *>(B2)[tid] = make_uint4(0, 0, 0, 0);
-        reinterpret_cast<uint4 *>(B3)[tid] = make_uint4(0, 0, 0, 0);
-      }
+      if (b2.x | b2.y | b2.z | b2.w) reinterpret_cast<uint4 *>(B2)[tid] = make_uint4(0, 0, 0, 0);
+      if (b3.x | b3.y | b3.z | b3.w) reinterpret_cast<uint4 *>(B3)[tid] = make_uint4(0, 0, 0, 0);
     }
     fence_proxy_async_smem();  // staging writes -> visible to the bulk copy
     named_sync<BLOCK>();       // S3

@@ -330,11 +330,14 @@ __global__ void __launch_bounds__(BLOCK, 1) hist16_kernel(Ws ws) {
   // input, with no per-key overflow test.
   constexpr int GPE = 32768 / (BLOCK * EPG);  // granules per thread per epoch
   static_assert(GPE % UNR == 0 && GPE > 0, "whole batches per epoch");
-  // A batch = UNR granules per thread.  The batch's OR/AND masks (which the
-  // root's masks need anyway) show when all of a thread's keys share one bin;
-  // when all 32 lanes share the same bin (sorted or constant runs) one add of
-  // 32*UNR*EPG replaces that many same-address atomics.  The epoch bound is
+  // A batch = UNR granules per thread (a warp's batch is contiguous).  The
+  // batch's OR/AND masks (which the root's masks need anyway) show when all of
+  // a thread's keys share one bin; when all 32 lanes share the same bin
+  // (sorted or constant runs) one add of 32*UNR*EPG replaces that many
+  // same-address atomics.  After a failed check the warp skips the check for
+  // 7 batches, so spread keys pay ~nothing for it.  The epoch bound is
   // unchanged (the same keys are counted).
+  int skip = 0;  // batches until the next same-bin check (warp-uniform)
   for (uint64_t eb = g0; eb < g1; eb += uint64_t(GPE) * BLOCK) {  // block-uniform epochs
 #pragma unroll
     for (int u0 = 0; u0 < GPE; u0 += UNR) {
@@ -381,11 +384,18 @@ __global__ void __launch_bounds__(BLOCK, 1) hist16_kernel(Ws ws) {
       o |= ob;
       a &= ab;
       constexpr uint32_t ALL = (1u << (UNR * EPG)) - 1u;
-      const uint32_t pb = (uint32_t(ob >> shA) & msk) << post;
-      const bool same = valid == ALL && ((uint32_t((ob ^ ab) >> shA) & msk) == 0u);
-      const uint32_t lead = __shfl_sync(0xFFFFFFFFu, pb, 0);
-      if (__all_sync(0xFFFFFFFFu, same && pb == lead)) {
-        if (lane == 0) atomicAdd(&hw[lead >> 1], (32u * UNR * EPG) << (16u * (lead & 1u)));
+      bool agg = false;
+      if (skip == 0) {  // warp-uniform
+        const uint32_t pb = (uint32_t(ob >> shA) & msk) << post;
+        const bool same = valid == ALL && ((uint32_t((ob ^ ab) >> shA) & msk) == 0u);
+        const uint32_t lead = __shfl_sync(0xFFFFFFFFu, pb, 0);
+        agg = __all_sync(0xFFFFFFFFu, same && pb == lead);
+        if (agg && lane == 0) atomicAdd(&hw[lead >> 1], (32u * UNR * EPG) << (16u * (lead & 1u)));
+        if (!agg) skip = 7;  // spread keys: look again 8 batches later
+      } else {
+        --skip;
+      }
+      if (agg) {
       } else if (valid == ALL) {
 #pragma unroll
         for (int i = 0; i < UNR * EPG; ++i) {

@@ -111,6 +111,7 @@ def main(argv=None):
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--only", default="")
     ap.add_argument("--out", default="")
+    ap.add_argument("--warmup", type=int, default=3)
     a = ap.parse_args(argv)
     names = ["cfg1", "cfg2", "cfg3_uniform", "cfg3_zipf", "cfg3_low16", "cfg4", "cfg5", "cfg5_sorted",
              "cfg5_reverse"]
@@ -121,7 +122,7 @@ def main(argv=None):
     res = []
     for nm in names:
         with Clocks(0) as clk:
-            r = run(nm, a.reps)
+            r = run(nm, a.reps, warmup=a.warmup)
         r["clocks"] = clk.summary()
         print(json.dumps(r), flush=True)
         res.append(r)
