@@ -113,7 +113,8 @@ static Geometry geometry(uint64_t n, int kb, int vb, int width_eff) {
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t ctl, buckets[2], bhist[2], bor[2], band[2], tile_bucket[2], status, hist16, h16part, tasks, dtasks, keys, vals, total;
+  size_t ctl, buckets[2], bhist[2], bor[2], band[2], tile_bucket[2], status, toff, hist16, h16part, tasks, dtasks, keys, vals,
+      total;
 };
 
 static Layout layout(const Geometry &g, bool own_copy = true) {
@@ -133,6 +134,7 @@ static Layout layout(const Geometry &g, bool own_copy = true) {
     l.tile_bucket[p] = take(sizeof(uint32_t) * g.maxtiles);
   }
   l.status = take(sizeof(uint32_t) * 256 * size_t(g.maxtiles));
+  l.toff = take(g.vb ? sizeof(uint32_t) * 256 * size_t(g.maxtiles) : 0);
   l.hist16 = take(sizeof(uint32_t) * 65536);
   l.h16part = take(sizeof(uint32_t) * 32768 * size_t(H16_MAXCTA));
   l.tasks = take(sizeof(Task) * g.maxtasks);
@@ -171,6 +173,7 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
     ws.tile_bucket[p] = reinterpret_cast<uint32_t *>(base + lay.tile_bucket[p]);
   }
   ws.status = reinterpret_cast<uint32_t *>(base + lay.status);
+  ws.toff = reinterpret_cast<uint32_t *>(base + lay.toff);
   ws.hist16 = reinterpret_cast<uint32_t *>(base + lay.hist16);
   ws.h16part = reinterpret_cast<uint32_t *>(base + lay.h16part);
   ws.tasks = reinterpret_cast<Task *>(base + lay.tasks);
@@ -252,7 +255,9 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   if (n > geo.local_max) {
     const int nlev = geo.ndig + 1;
     for (int L = 0; L < nlev; ++L) {
-      if (L == 0) {
+      // keys-only: level 0 counts digit pairs (hist16), so level 1 needs no
+      // histogram pass; stable sorts count per tile at every level instead
+      if (L == 0 && VB == 0) {
         const int parts = num_sms() < H16_MAXCTA ? num_sms() : H16_MAXCTA;
         BS_CUDA(pdl_launch(h16, parts, H16_BLOCK, H16_SMEM, st, ws));
         BS_CUDA(pdl_launch(hist16_reduce_kernel, 32768 / 4 / 64, 256, 0, st, ws, parts));
@@ -260,6 +265,7 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
       else BS_CUDA(pdl_launch(hk, hk_grid, HI_BLOCK, 0, st, ws, L));
       mark(st);
       BS_CUDA(pdl_launch(plan_kernel<K>, num_sms() * 4, 256, 0, st, ws, L));
+      if constexpr (VB != 0) BS_CUDA(pdl_launch(tile_scan_kernel, num_sms() * 8, 256, 0, st, ws, L));
       mark(st);
       if constexpr (WSPEC) BS_CUDA(pdl_launch(sw, sc_grid, SC_BLOCK + 32, SW::bytes, st, ws, L));
       else BS_CUDA(pdl_launch(sc, sc_grid, SC_BLOCK, SS::bytes, st, ws, L));

@@ -87,6 +87,7 @@ struct Ctl {
   uint32_t nbuckets[MAXLEV + 1];
   uint32_t ntiles[MAXLEV + 1];
   uint32_t ticket[MAXLEV + 1];
+  uint32_t ticket2[MAXLEV + 1];  // tile_scan_kernel
   uint32_t ntasks;
   uint32_t ndtasks;      // small dense tasks (front of dtasks)
   uint32_t error;        // bit 0: bucket overflow, 1: tile overflow, 2: task overflow
@@ -103,7 +104,8 @@ struct Ws {
   uint64_t *bor[2];
   uint64_t *band[2];
   uint32_t *tile_bucket[2];
-  uint32_t *status;  // [maxtiles][256]
+  uint32_t *status;  // [maxtiles][256] look-back words (stable sorts)
+  uint32_t *toff;    // [maxtiles][256] stable sorts: tile digit counts, then run offsets
   uint32_t *hist16;  // [65536]: root histogram of the digit pair (dig, dig+1)
   uint32_t *h16part; // [H16_MAXCTA][32768]: per-CTA packed partial rows
   Task *tasks;
@@ -197,6 +199,7 @@ __global__ void __launch_bounds__(BLOCK) hist_kernel(Ws ws, int L) {
   constexpr int NCOPY = 4;
   __shared__ uint32_t h[NCOPY][256];
   __shared__ uint64_t s_or[BLOCK / 32], s_and[BLOCK / 32];
+  __shared__ uint32_t tprev[256];  // stable sorts: bucket counts up to the previous tile
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int cur = L & 1;
   const uint32_t nt = ws.ctl->ntiles[L];
@@ -207,6 +210,7 @@ __global__ void __launch_bounds__(BLOCK) hist_kernel(Ws ws, int L) {
   if (t0 >= t1) return;
   const KeyGeom<K, KIND> g{ws.shift0};
   for (int i = tid; i < NCOPY * 256; i += BLOCK) (&h[0][0])[i] = 0;
+  for (int i = tid; i < 256; i += BLOCK) tprev[i] = 0;
   K o = 0, a = ~K(0);
   uint32_t curb = 0xFFFFFFFFu;
   int dig = 0;
@@ -221,6 +225,7 @@ __global__ void __launch_bounds__(BLOCK) hist_kernel(Ws ws, int L) {
         s += h[c][d];
         h[c][d] = 0;
       }
+      tprev[d] = 0;
       if (s) atomicAdd(&ws.bhist[cur][size_t(b) * 256 + d], s);
     }
     K oo = warp_or(o), aa = warp_and(a);
@@ -274,6 +279,17 @@ __global__ void __launch_bounds__(BLOCK) hist_kernel(Ws ws, int L) {
         a &= nk;
         atomicAdd(&hc[KeyGeom<K, KIND>::digit_of_norm(nk, dig)], 1u);
       }
+    }
+    if (ws.stable) {  // this tile's own digit counts, for tile_scan_kernel
+      __syncthreads();
+      for (int d = tid; d < 256; d += BLOCK) {
+        uint32_t cur = 0;
+#pragma unroll
+        for (int cc = 0; cc < NCOPY; ++cc) cur += h[cc][d];
+        ws.toff[size_t(t) * 256 + d] = cur - tprev[d];
+        tprev[d] = cur;
+      }
+      __syncthreads();
     }
   }
   if (!known) flush(curb);
@@ -601,7 +617,7 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
     const uint32_t cpar = bk.parity ^ 1u;
     const int lowbits = W - 8 - 8 * dig;
     // the root's children take their histograms from hist16 (no hist pass at level 1)
-    const bool h16 = L == 0 && ws.ctl->h16_bad == 0u;
+    const bool h16 = L == 0 && ws.ctl->h16_bad == 0u && !ws.stable;
     const K lower = lowbits > 0 ? (var & ((K(1) << lowbits) - 1)) : K(0);
     if (lower == 0) {  // every child is all-equal: only a copy home may remain
       if (tid == 0 && cpar) emit_tasks(ws, bk.start, bk.count, 1);
@@ -958,6 +974,75 @@ __device__ __forceinline__ void issue_copy(const Ws &ws, unsigned char *dbuf, ui
 }
 
 // ---------------------------------------------------------------------------
+// Stable sorts: per-tile digit run offsets, computed ahead of the scatter from
+// the tiles' digit counts (hist_kernel wrote them to toff).  A CTA claims a
+// block of TS_T consecutive tiles (ticket order), runs a per-digit sum over
+// them that restarts at every bucket start, publishes its last segment's
+// total (inclusive if that segment's bucket starts inside the block), and --
+// if its first segment continues a bucket from earlier blocks -- looks back
+// over the earlier blocks' publications (decoupled look-back) for the carry.
+// Result: toff[t][d] = digit base in the bucket + number of digit-d elements
+// in the bucket's earlier tiles.  Only 1 KB per tile moves and the chain is
+// one step per TS_T tiles, so the scatter itself needs no cross-tile wait.
+// ---------------------------------------------------------------------------
+constexpr int TS_T = 32;  // tiles per tile_scan block
+
+__global__ void __launch_bounds__(256) tile_scan_kernel(Ws ws, int L) {
+  pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
+  __shared__ uint32_t s_blk;
+  __shared__ uint32_t s_b[TS_T], s_start[TS_T];  // tile's bucket; tile starts its bucket
+  const int d = threadIdx.x;
+  const int lv = L & 1;
+  const uint32_t nt = ws.ctl->ntiles[L];
+  for (;;) {
+    if (d == 0) s_blk = atomicAdd(&ws.ctl->ticket2[L], 1u);
+    __syncthreads();
+    const uint32_t blk = s_blk;
+    const uint32_t t0 = blk * TS_T;
+    if (t0 >= nt) return;
+    const uint32_t t1 = min(nt, t0 + uint32_t(TS_T));
+    if (d < TS_T && t0 + d < t1) {
+      const uint32_t b = ws.tile_bucket[lv][t0 + d];
+      s_b[d] = b;
+      s_start[d] = ws.buckets[lv][b].tile0 == t0 + d ? 1u : 0u;
+    }
+    uint32_t c[TS_T];  // all loads in flight at once
+#pragma unroll
+    for (int i = 0; i < TS_T; ++i) c[i] = t0 + i < t1 ? ws.toff[size_t(t0 + i) * 256 + d] : 0u;
+    __syncthreads();
+    const bool open_first = s_start[0] == 0u;  // the first segment continues a bucket from earlier blocks
+    uint32_t first_end = t1 - t0;             // tiles [0, first_end) continue the first segment
+    uint32_t run = 0;
+#pragma unroll
+    for (int i = 0; i < TS_T; ++i) {
+      if (t0 + i < t1) {
+        if (s_start[i]) {
+          if (i > 0 && first_end == t1 - t0) first_end = uint32_t(i);
+          run = 0;
+        }
+        const uint32_t x = c[i];
+        c[i] = run;
+        run += x;
+      }
+    }
+    uint32_t *st = ws.status + size_t(blk) * 256 + d;
+    const bool chained = open_first && first_end == t1 - t0;  // one open segment: needs the carry
+    st_relaxed(st, (chained ? ST_AGG : ST_INCL) | run);
+    uint32_t carry = 0;
+    if (open_first) {
+      carry = lookback(ws.status, blk, 0, d);
+      if (chained) st_relaxed(st, ST_INCL | (carry + run));
+    }
+#pragma unroll
+    for (int i = 0; i < TS_T; ++i)
+      if (t0 + i < t1)
+        ws.toff[size_t(t0 + i) * 256 + d] =
+            c[i] + ws.bhist[lv][size_t(s_b[i]) * 256 + d] + (uint32_t(i) < first_end ? carry : 0u);
+    __syncthreads();  // s_b / s_start / s_blk are reused by the next block
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K2+K3: scatter one digit with single-pass decoupled look-back.  Persistent
 // CTAs claim tiles in order; the next tile is bulk-copied (TMA) into the
 // spare buffer while the current one is ranked, scanned and scattered; the
@@ -1038,20 +1123,20 @@ __global__ void __launch_bounds__(BLOCK) scatter_kernel(Ws ws, int L) {
   BS_PROBE_INIT();
   int cur = 0;
   for (;;) {
-    // keys-only tiles have no look-back, so the next tile is claimed (and
-    // its bulk copy started) as early as possible
-    if (!STABLE && tid == 0) claim(cur ^ 1);
     if constexpr (STABLE) {
 #pragma unroll
       for (int i = lane; i < 256; i += 32) whist[i] = 0;
     } else {
       if (tid < 256) whist[tid] = 0;
     }
-    __syncthreads();
+    __syncthreads();  // the previous tile's write-out has left buffer cur^1
+    // no look-back inside the scatter (tile offsets are precomputed for
+    // stable sorts), so the next tile is claimed (and its bulk copy started)
+    // as early as possible
+    if (tid == 0) claim(cur ^ 1);
     const InFlight f = info[cur];
     if (f.idx >= nt) break;
     if (!f.valid) {
-      if (STABLE && tid == 0) claim(cur ^ 1);
       __syncthreads();
       cur ^= 1;
       continue;
@@ -1116,21 +1201,14 @@ __global__ void __launch_bounds__(BLOCK) scatter_kernel(Ws ws, int L) {
       // so the offsets come from a single-pass chained scan with decoupled
       // look-back.  Publish this tile's counts first so successors can look
       // past it.
-      uint32_t *st = ws.status + size_t(f.idx) * 256 + tid;
-      if (tid < 256) st_relaxed(st, (f.tin == 0 ? ST_INCL : ST_AGG) | total);
       texcl = scan256_excl<BLOCK>(total, misc);
       BS_PROBE(3);
       if (tid < 256) {
         tstart[tid] = texcl;
-        uint32_t prefix = 0;
-        if (f.tin != 0) {
-          prefix = lookback(ws.status, f.idx, f.tile0, tid);
-          st_relaxed(st, ST_INCL | (prefix + total));
-        }
         // element offset of this tile's digit-d run minus its tile position
-        // (mod 2^32: true offsets are < n <= 2^30)
-        reinterpret_cast<uint32_t *>(gbase)[tid] =
-            bucket_start + ws.bhist[lv][size_t(f.b) * 256 + tid] + prefix - texcl;
+        // (tile_scan_kernel: digit base + earlier tiles' digit-d counts;
+        // mod 2^32: true offsets are < n <= 2^30)
+        reinterpret_cast<uint32_t *>(gbase)[tid] = bucket_start + ws.toff[size_t(f.idx) * 256 + tid] - texcl;
       }
     } else {
       // Keys-only MSD: the order of keys inside a child bucket is irrelevant
@@ -1166,9 +1244,6 @@ __global__ void __launch_bounds__(BLOCK) scatter_kernel(Ws ws, int L) {
     }
     __syncthreads();
     BS_PROBE(5);
-    // Stable sorts claim the next tile only now: a claimed-but-unranked tile
-    // would stall its successors' look-back.  Its copy overlaps this write-out.
-    if (STABLE && tid == 0) claim(cur ^ 1);
     K *dst = static_cast<K *>(ws.keys[f.parity ^ 1]);
     V *vdst = VB ? static_cast<V *>(ws.vals[f.parity ^ 1]) : nullptr;
     const uint32_t *gb = reinterpret_cast<const uint32_t *>(gbase);
