@@ -1607,13 +1607,9 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
     }
     __syncthreads();
     K var, common;
-    {
-      K oo = 0, aa = ~K(0);
-#pragma unroll
-      for (int i = 0; i < S::NW; ++i) {
-        oo |= K(red[i]);
-        aa &= K(red[S::NW + i]);
-      }
+    {  // every warp folds the per-warp masks with shuffles (not NW loads per thread)
+      const K oo = warp_or(lane < S::NW ? K(red[lane]) : K(0));
+      const K aa = warp_and(lane < S::NW ? K(red[S::NW + lane]) : ~K(0));
       var = oo ^ aa;
       common = oo;
     }
@@ -1712,16 +1708,17 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
         // else: too many repeats for the overflow list -> LSD passes below
       }
       // Bin sort (keys only, any span): one counting pass on the top B varying
-      // bits with 2^B >= n bins (about one key per bin), then every key finds
-      // its place inside its bin by comparing itself with the bin's few other
-      // keys -- one shared atomic, two scattered stores and ~2 loads per key
-      // instead of one ranking pass per varying digit.  A task with a bin of
-      // more than BIN_MAX keys (heavy duplicates) takes the LSD passes below.
+      // bits with 2^B >= 2n bins (about half a key per bin), then every key
+      // finds its place inside its bin by comparing itself with the bin's few
+      // other keys -- one shared atomic, two scattered stores and ~2 loads per
+      // key instead of one ranking pass per varying digit.  The in-bin ranking
+      // costs sum(c^2) comparisons over the bin sizes c (~1.5n for spread
+      // keys); a task above 8n (heavy duplicates) takes the LSD passes below.
       if (!done && n >= 64) {
         constexpr int BIN_LOG_MAX = 13;  // 8192 counters fit the bitmap region
         static_assert(sizeof(uint32_t) * (1u << BIN_LOG_MAX) <= S::bm_bytes, "bins fit");
         const int hb = W - 1 - KeyTraits<K>::clz(var);  // top varying bit of the normalised key
-        int B = 32 - __clz(uint32_t(n - 1));
+        int B = 33 - __clz(uint32_t(n - 1));  // about two bins per key: short in-bin loops
         B = min(min(B, BIN_LOG_MAX), hb + 1);
         const int sh = hb + 1 - B;
         const uint32_t nbins = 1u << B, bmask = nbins - 1u;
@@ -1738,11 +1735,11 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
         __syncthreads();
         const uint32_t bpt = (nbins + BLOCK - 1) / BLOCK;
         const uint32_t q0 = min(nbins, uint32_t(tid) * bpt), q1 = min(nbins, q0 + bpt);
+        const bool vec = (bpt & 3u) == 0u;  // whole uint4 chunks (conflict-free scan loads)
         if (tid == 0) misc[48] = 0;
-        uint32_t c = 0, c2 = 0;
-        for (uint32_t q = q0; q < q1; ++q) {
+        uint32_t c2 = 0;
+        for (uint32_t q = tid; q < nbins; q += BLOCK) {  // strided: conflict-free
           const uint32_t v = bins[q];
-          c += v;
           c2 += v * v;
         }
         __syncthreads();
@@ -1750,11 +1747,33 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
         if (lane == 0 && c2) atomicAdd(&misc[48], c2);
         __syncthreads();
         if (misc[48] <= 8u * uint32_t(n)) {
+          uint4 *b4 = reinterpret_cast<uint4 *>(bins);
+          uint32_t c = 0;
+          if (vec) {
+            for (uint32_t q = q0 / 4; q < q1 / 4; ++q) {
+              const uint4 v = b4[q];
+              c += v.x + v.y + v.z + v.w;
+            }
+          } else {
+            for (uint32_t q = q0; q < q1; ++q) c += bins[q];
+          }
           uint32_t run = block_scan_excl<BLOCK>(c, misc);
-          for (uint32_t q = q0; q < q1; ++q) {
-            const uint32_t v = bins[q];
-            bins[q] = run;
-            run += v;
+          if (vec) {
+            for (uint32_t q = q0 / 4; q < q1 / 4; ++q) {
+              const uint4 v = b4[q];
+              uint4 o;
+              o.x = run, run += v.x;
+              o.y = run, run += v.y;
+              o.z = run, run += v.z;
+              o.w = run, run += v.w;
+              b4[q] = o;
+            }
+          } else {
+            for (uint32_t q = q0; q < q1; ++q) {
+              const uint32_t v = bins[q];
+              bins[q] = run;
+              run += v;
+            }
           }
           __syncthreads();
           // bin order (arbitrary inside a bin)
@@ -1776,10 +1795,11 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
               const uint32_t s = bins[d], e = d < bmask ? bins[d + 1] : uint32_t(n);
               const uint32_t p = s + slot.get(j);
               uint32_t r = 0;
-              for (uint32_t i = s; i < e; ++i) {
-                const K y = g.norm(kb[i]);
-                r += (y < nk || (y == nk && i < p)) ? 1u : 0u;
-              }
+              if (e - s > 1u)  // most keys are alone in their bin
+                for (uint32_t i = s; i < e; ++i) {
+                  const K y = g.norm(kb[i]);
+                  r += (y < nk || (y == nk && i < p)) ? 1u : 0u;
+                }
               fin.set(j, s + r);
             }
           }
