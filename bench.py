@@ -38,6 +38,17 @@ N_KEYS = 1 << 28
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 
 
+def _traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu launch list summary
+    (profiles/traffic.json: dram__bytes_read.sum + dram__bytes_write.sum), or None."""
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")) as fh:
+            t = json.load(fh)[kernel]
+        return int(t["dram_read_bytes"] + t["dram_write_bytes"])
+    except Exception:
+        return None
+
+
 def _peaks():
     try:
         with open(PEAKS_PATH) as fh:
@@ -305,10 +316,14 @@ def run_gpu(args):
         "vs_baseline": None, "dtype": "u32", "data": "synthetic (MT19937 seed 1+rank, cfg2 stream)",
         "config": {"workload": "cfg2: 2^28 uint32 keys/rank, uniform from MT19937(1+rank), keys only, sort ascending",
                    "global_batch": total_keys, "keys_per_rank": n,
-                   "parallelism": "single GPU" if world == 1 else f"range-partition x{world} + NCCL all-to-all-v",
+                   "parallelism": "single GPU" if world == 1 else
+                   f"range-partition x{world}: fused partition + NVLink peer stores (CUDA IPC), NCCL for counts",
                    "l2": "inputs 1 GiB > 126 MB L2; pristine copy restored between steps (outside events)"},
         "clocks": clocks,
-        "gpu_launches": int(L.bs_sort_launches(n, 4, 32, 0, 0)) * args.steps if world == 1 else None,
+        # our kernels per step; N>1: sample, sample sort, class count (4), fused exchange, local sort
+        "gpu_launches": (int(L.bs_sort_launches(n, 4, 32, 0, 0)) if world == 1 else
+                         1 + int(L.bs_sort_launches(world * 4096, 4, 32, 0, 0)) + 5 +
+                         int(L.bs_sort_launches(n, 4, 32, 0, 0))) * args.steps,
     }
     if world == 1:
         # phases: [init, (hist, plan, scatter) x nlev, local]
@@ -318,6 +333,7 @@ def run_gpu(args):
         for k, v in avg.items():
             kinds[k.rstrip("0123456789")] += v
         dominant = max(("scatter", "local", "hist"), key=lambda k: kinds[k])
+        kname = {"scatter": "scatter_ws_kernel", "local": "dense_kernel", "hist": "hist16_kernel"}[dominant]
         if dominant == "scatter":
             durs = [avg[f"scatter{lv}"] for lv in range(nlev) if avg.get(f"scatter{lv}", 0) > 0.05]
             alg = 2 * 4 * n
@@ -329,8 +345,9 @@ def run_gpu(args):
             alg = 4 * n
         kms = sum(durs) / len(durs)
         achieved = alg / (kms / 1e3) / 1e9
-        line["roofline"] = {"bound": "hbm", "kernel": f"{dominant}_kernel", "achieved": achieved, "peak": peak,
-                            "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+        line["roofline"] = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
+                            "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                            "traffic": _traffic(kname), "traffic_unit": "bytes per launch (ncu dram read+write)",
                             "alg_bytes_per_launch": alg, "avg_launch_ms": kms, "launches_averaged": len(durs)}
         t_roof = bpk * n / (peak * 1e9)
         line["sort_roofline"] = {"p_alg": p_alg, "alg_bytes": bpk * n, "t_roof_ms": t_roof * 1e3,

@@ -1711,9 +1711,10 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
       // bits with 2^B >= 2n bins (about half a key per bin), then every key
       // finds its place inside its bin by comparing itself with the bin's few
       // other keys -- one shared atomic, two scattered stores and ~2 loads per
-      // key instead of one ranking pass per varying digit.  The in-bin ranking
-      // costs sum(c^2) comparisons over the bin sizes c (~1.5n for spread
-      // keys); a task above 8n (heavy duplicates) takes the LSD passes below.
+      // key instead of one ranking pass per varying digit.  A bin whose keys
+      // are all equal ranks them by arrival; the mixed bins cost sum(c^2)
+      // comparisons over their sizes c (~1.5n for spread keys); a task above
+      // 8n takes the LSD passes below.
       if (!done && n >= 64) {
         constexpr int BIN_LOG_MAX = 13;  // 8192 counters fit the bitmap region
         static_assert(sizeof(uint32_t) * (1u << BIN_LOG_MAX) <= S::bm_bytes, "bins fit");
@@ -1736,17 +1737,19 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
         const uint32_t bpt = (nbins + BLOCK - 1) / BLOCK;
         const uint32_t q0 = min(nbins, uint32_t(tid) * bpt), q1 = min(nbins, q0 + bpt);
         const bool vec = (bpt & 3u) == 0u;  // whole uint4 chunks (conflict-free scan loads)
+        // comparisons a plain in-bin ranking needs: sum of c^2 over all bins
         if (tid == 0) misc[48] = 0;
-        uint32_t c2 = 0;
-        for (uint32_t q = tid; q < nbins; q += BLOCK) {  // strided: conflict-free
-          const uint32_t v = bins[q];
-          c2 += v * v;
+        {
+          uint32_t c2 = 0;
+          for (uint32_t q = tid; q < nbins; q += BLOCK) {  // strided: conflict-free
+            const uint32_t v = bins[q];
+            c2 += v * v;
+          }
+          __syncthreads();
+          c2 = __reduce_add_sync(0xFFFFFFFFu, c2);
+          if (lane == 0 && c2) atomicAdd(&misc[48], c2);
         }
-        __syncthreads();
-        c2 = __reduce_add_sync(0xFFFFFFFFu, c2);
-        if (lane == 0 && c2) atomicAdd(&misc[48], c2);
-        __syncthreads();
-        if (misc[48] <= 8u * uint32_t(n)) {
+        {
           uint4 *b4 = reinterpret_cast<uint4 *>(bins);
           uint32_t c = 0;
           if (vec) {
@@ -1775,14 +1778,45 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
               run += v;
             }
           }
-          __syncthreads();
-          // bin order (arbitrary inside a bin)
+        }
+        const bool spread = misc[48] <= 8u * uint32_t(n);  // (block_scan synced)
+        __syncthreads();
+        if (tid == 0) misc[48] = 0;
+        // bin order (arbitrary inside a bin)
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+          if (j >= kk) break;
+          if (32 * j + lane < nvw) kb[bins[uint32_t(g.norm(x[j]) >> sh) & bmask] + slot.get(j)] = x[j];
+        }
+        __syncthreads();
+        // Duplicate-heavy tasks: a bin is "pure" when all its keys equal its
+        // first one; its keys rank by arrival, no comparisons.  Flag the mixed
+        // bins and count only their comparisons.
+        constexpr uint32_t MIXED = 0x80000000u, OFF = 0x7FFFFFFFu;
+        if (!spread) {
 #pragma unroll
           for (int j = 0; j < KPT; ++j) {
             if (j >= kk) break;
-            if (32 * j + lane < nvw) kb[bins[uint32_t(g.norm(x[j]) >> sh) & bmask] + slot.get(j)] = x[j];
+            if (32 * j + lane < nvw) {
+              const uint32_t d = uint32_t(g.norm(x[j]) >> sh) & bmask;
+              const uint32_t s0 = bins[d] & OFF;
+              if (kb[s0] != x[j]) atomicOr(&bins[d], MIXED);
+            }
           }
           __syncthreads();
+          uint32_t c2 = 0;
+          for (uint32_t q = tid; q < nbins; q += BLOCK) {  // strided: conflict-free
+            const uint32_t bq = bins[q];
+            if (bq & MIXED) {
+              const uint32_t c = (q < bmask ? (bins[q + 1] & OFF) : uint32_t(n)) - (bq & OFF);
+              c2 += c * c;
+            }
+          }
+          c2 = __reduce_add_sync(0xFFFFFFFFu, c2);
+          if (lane == 0 && c2) atomicAdd(&misc[48], c2);
+          __syncthreads();
+        }
+        if (spread || misc[48] <= 8u * uint32_t(n)) {
           // place inside the bin: smaller keys, then equal keys that arrived earlier
           Ranks<KPT> fin;
           fin.clear();
@@ -1792,15 +1826,19 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
             if (32 * j + lane < nvw) {
               const K nk = g.norm(x[j]);
               const uint32_t d = uint32_t(nk >> sh) & bmask;
-              const uint32_t s = bins[d], e = d < bmask ? bins[d + 1] : uint32_t(n);
-              const uint32_t p = s + slot.get(j);
+              const uint32_t bd = bins[d], s0 = bd & OFF;
+              const uint32_t e = d < bmask ? (bins[d + 1] & OFF) : uint32_t(n);
+              const uint32_t p = s0 + slot.get(j);
               uint32_t r = 0;
-              if (e - s > 1u)  // most keys are alone in their bin
-                for (uint32_t i = s; i < e; ++i) {
+              if (spread ? e - s0 <= 1u : !(bd & MIXED)) {
+                r = slot.get(j);  // alone, or all equal: arrival order
+              } else {
+                for (uint32_t i = s0; i < e; ++i) {
                   const K y = g.norm(kb[i]);
                   r += (y < nk || (y == nk && i < p)) ? 1u : 0u;
                 }
-              fin.set(j, s + r);
+              }
+              fin.set(j, s0 + r);
             }
           }
           __syncthreads();
