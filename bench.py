@@ -223,12 +223,21 @@ def run_gpu(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: BS_BENCH_SHARE_GPU=1 puts every rank on cuda:0 (gloo for the
+    # host collectives) to exercise the N>1 path on a one-GPU box; never a
+    # measurement (kernels of different ranks time-share one GPU)
+    share = os.environ.get("BS_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     from paper_0811_3448_b200 import UnsignedCodec, _lib, device, sort
     from paper_0811_3448_b200.cases import mt_words
 
@@ -276,6 +285,28 @@ def run_gpu(args):
         if not ok:
             print("bench: GPU output differs from np.sort", file=sys.stderr)
             return 1
+    else:  # this rank's slice sorted, slices in rank order, nothing lost
+        import torch.distributed as dist
+
+        k = r.keys.to(torch.int64) & 0xFFFFFFFF
+        ok = bool((k[1:] >= k[:-1]).all()) if k.numel() > 1 else True
+        ends = torch.tensor([k.numel(), int(k[0]) if k.numel() else -1, int(k[-1]) if k.numel() else -1],
+                            dtype=torch.int64, device="cpu" if share else dev)
+        allends = [torch.empty_like(ends) for _ in range(world)]
+        dist.all_gather(allends, ends)
+        e = [[int(v) for v in t.cpu()] for t in allends]
+        ok = ok and sum(x[0] for x in e) == n * world
+        last = -1
+        for cnt, lo, hi in e:
+            if cnt:
+                ok = ok and lo >= last
+                last = hi
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int64, device="cpu" if share else dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)  # every rank takes the same exit
+        if int(flag.item()) == 0:
+            print(f"bench: rank {rank}: distributed output not globally sorted", file=sys.stderr)
+            dist.destroy_process_group()
+            return 1
 
     phase = [[] for _ in range(nev)]
     step_ms = []
@@ -304,7 +335,7 @@ def run_gpu(args):
     if world > 1:
         import torch.distributed as dist
 
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms], dtype=torch.float64, device="cpu" if share else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     total_keys = n * world
@@ -314,7 +345,8 @@ def run_gpu(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic (MT19937 seed 1+rank, cfg2 stream)",
-        "config": {"workload": "cfg2: 2^28 uint32 keys/rank, uniform from MT19937(1+rank), keys only, sort ascending",
+        "config": {"workload": (f"cfg2: 2^{n.bit_length() - 1}" if n & (n - 1) == 0 else f"cfg2-shaped: {n}") +
+                               " uint32 keys/rank, uniform from MT19937(1+rank), keys only, sort ascending",
                    "global_batch": total_keys, "keys_per_rank": n,
                    "parallelism": "single GPU" if world == 1 else
                    f"range-partition x{world}: fused partition + NVLink peer stores (CUDA IPC), NCCL for counts",
@@ -402,7 +434,7 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=N_KEYS, help="keys per rank (default 2^28 = cfg2)")
+    ap.add_argument("--keys-per-rank", "--n", dest="n", type=int, default=N_KEYS, help="keys per rank (default 2^28 = cfg2)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -180,3 +180,23 @@ def test_two_processes_peer_exchange_one_gpu():
         order = np.argsort(allk, kind="stable")
         assert np.array_equal(outk, allk[order])
         assert np.array_equal(outv, allv[order])
+
+
+@pytest.mark.timeout(600)
+def test_bench_two_ranks_share_one_gpu():
+    """bench.py's N>1 path (torchrun, dist_sort with the fused peer exchange,
+    global-order check, max-over-ranks timing) with both ranks on cuda:0."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, BS_BENCH_SHARE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
+           "--steps", "2", "--warmup", "3", "--keys-per-rank", str(1 << 22)]
+    p = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=500)
+    assert p.returncode == 0, p.stderr[-2000:]
+    line = [ln for ln in p.stdout.splitlines() if ln.startswith("{")][-1]
+    r = json.loads(line)
+    assert r["n_gpus"] == 2 and r["config"]["global_batch"] == 2 << 22 and r["value"] > 0
