@@ -89,6 +89,19 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
+// atomicOr on shared memory issued under a predicate (no branch around it);
+// returns the old word, or 0 when `on` is false
+__device__ __forceinline__ uint32_t atom_or_shared_if(uint32_t *p, uint32_t v, bool on) {
+  uint32_t old = 0;
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q atom.shared.or.b32 %0, [%1], %2;\n\t}"
+      : "+r"(old)
+      : "r"(a), "r"(v), "r"(uint32_t(on))
+      : "memory");
+  return old;
+}
+
 __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

@@ -199,9 +199,8 @@ __global__ void __launch_bounds__(BLOCK + 32, BIG ? 1 : 2) dense_kernel(Ws ws, i
         uint32_t third = 0;
 #pragma unroll
         for (int j = 0; j < EPG; ++j) {
-          const uint32_t bit = ((rep >> j) & 1u) << (idx[j] & 31u);
-          if (rep & (1u << j))
-            if (atomicOr(&B2[idx[j] >> 5], bit) & bit) third |= 1u << j;
+          const uint32_t bit = 1u << (idx[j] & 31u);
+          if (atom_or_shared_if(&B2[idx[j] >> 5], bit, (rep >> j) & 1u) & bit) third |= 1u << j;
         }
         if (third) {
 #pragma unroll
