@@ -1276,7 +1276,8 @@ __global__ void __launch_bounds__(BLOCK) scatter_kernel(Ws ws, int L) {
 // ---------------------------------------------------------------------------
 // Keys-only scatter, warp-specialised.  One producer warp claims tiles and
 // streams them in with TMA bulk copies through a ring of NBUF shared buffers
-// (full/empty mbarriers); BLOCK consumer threads rank (shared atomics),
+// (full/empty mbarriers); BLOCK consumer threads rank (shared atomics that
+// return each key's slot in its digit, warp-aggregated for skewed warps),
 // reserve each digit run with one global atomic per digit, stage the tile in
 // digit order in the consumed buffer and write it out coalesced.  Claim
 // latency and copy latency both hide behind the consumers' work.
@@ -1323,7 +1324,7 @@ __device__ __forceinline__ uint32_t scan256_excl_nb(uint32_t v, uint32_t *scratc
 }
 
 template <typename K, int KIND, int BLOCK, int KPT, int NBUF>
-__global__ void __launch_bounds__(BLOCK + 32) scatter_ws_kernel(Ws ws, int L) {
+__global__ void __launch_bounds__(BLOCK + 32, BLOCK >= 512 ? 2 : 3) scatter_ws_kernel(Ws ws, int L) {
   pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
   using S = ScatterWsSmem<K, KIND, BLOCK, KPT, NBUF>;
   constexpr int TILE = S::TILE;
@@ -1397,33 +1398,37 @@ __global__ void __launch_bounds__(BLOCK + 32) scatter_ws_kernel(Ws ws, int L) {
       const bool fullt = cnt == TILE;
       if (tid < 256) cnt256[tid] = 0;
       named_sync<BLOCK>();
-      // count (shared RED), scan, then place by atomic cursors -- no ranks
-      // kept in registers, no per-key lookup of the tile digit start
+      // count with shared atomics that return each key's arrival slot within
+      // its digit, scan, then place at tile digit start + slot (a plain load
+      // of the start instead of a second read-modify-write per key)
       K x[KPT];
+      Ranks<KPT> rk;
+      rk.clear();
       // A warp whose 32 keys share one digit (sorted or heavily skewed input)
       // does one aggregated atomic instead of 32 same-address ones.
       // The check costs a shuffle and a vote per key, so a warp only uses it
       // when its first 32 keys already share a digit.
-      bool skew = false;
       if (fullt) {
 #pragma unroll
         for (int j = 0; j < KPT; ++j) x[j] = kb[f.headk + j * BLOCK + tid];
         const uint32_t e0 = dfn(x[0]);
-        skew = __all_sync(0xFFFFFFFFu, e0 == __shfl_sync(0xFFFFFFFFu, e0, 0));
+        const bool skew = __all_sync(0xFFFFFFFFu, e0 == __shfl_sync(0xFFFFFFFFu, e0, 0));
         if (skew) {
 #pragma unroll
           for (int j = 0; j < KPT; ++j) {
             const uint32_t d = dfn(x[j]);
             const uint32_t d0 = __shfl_sync(0xFFFFFFFFu, d, 0);
             if (__all_sync(0xFFFFFFFFu, d == d0)) {
-              if (lane == 0) atomicAdd(&cnt256[d0], 32u);
+              uint32_t b0 = 0;
+              if (lane == 0) b0 = atomicAdd(&cnt256[d0], 32u);
+              rk.set(j, __shfl_sync(0xFFFFFFFFu, b0, 0) + uint32_t(lane));
             } else {
-              atomicAdd(&cnt256[d], 1u);
+              rk.set(j, atomicAdd(&cnt256[d], 1u));
             }
           }
         } else {
 #pragma unroll
-          for (int j = 0; j < KPT; ++j) atomicAdd(&cnt256[dfn(x[j])], 1u);
+          for (int j = 0; j < KPT; ++j) rk.set(j, atomicAdd(&cnt256[dfn(x[j])], 1u));
         }
       } else {
 #pragma unroll
@@ -1432,7 +1437,7 @@ __global__ void __launch_bounds__(BLOCK + 32) scatter_ws_kernel(Ws ws, int L) {
           x[j] = 0;
           if (e < cnt) {
             x[j] = kb[f.headk + e];
-            atomicAdd(&cnt256[dfn(x[j])], 1u);
+            rk.set(j, atomicAdd(&cnt256[dfn(x[j])], 1u));
           }
         }
       }
@@ -1442,32 +1447,17 @@ __global__ void __launch_bounds__(BLOCK + 32) scatter_ws_kernel(Ws ws, int L) {
       if (tid < 256 && total) base = atomicAdd(&ws.bhist[lv][size_t(f.b) * 256 + tid], total);
       const uint32_t texcl = scan256_excl_nb<BLOCK>(total, misc);
       if (tid < 256) {
-        tstart[tid] = texcl;  // becomes the staging cursor of digit tid
+        tstart[tid] = texcl;
         gbase[tid] = uint32_t(f.start - uint64_t(f.tin) * TILE) + base - texcl;
       }
       named_sync<BLOCK>();
-      if (fullt && !skew) {
+      if (fullt) {
 #pragma unroll
-        for (int j = 0; j < KPT; ++j) kb[atomicAdd(&tstart[dfn(x[j])], 1u)] = x[j];
-      } else if (fullt) {
-#pragma unroll
-        for (int j = 0; j < KPT; ++j) {
-          const uint32_t d = dfn(x[j]);
-          const uint32_t d0 = __shfl_sync(0xFFFFFFFFu, d, 0);
-          uint32_t pos;
-          if (__all_sync(0xFFFFFFFFu, d == d0)) {
-            uint32_t b0 = 0;
-            if (lane == 0) b0 = atomicAdd(&tstart[d0], 32u);
-            pos = __shfl_sync(0xFFFFFFFFu, b0, 0) + uint32_t(lane);
-          } else {
-            pos = atomicAdd(&tstart[d], 1u);
-          }
-          kb[pos] = x[j];
-        }
+        for (int j = 0; j < KPT; ++j) kb[tstart[dfn(x[j])] + rk.get(j)] = x[j];
       } else {
 #pragma unroll
         for (int j = 0; j < KPT; ++j)
-          if (j * BLOCK + tid < cnt) kb[atomicAdd(&tstart[dfn(x[j])], 1u)] = x[j];
+          if (j * BLOCK + tid < cnt) kb[tstart[dfn(x[j])] + rk.get(j)] = x[j];
       }
       named_sync<BLOCK>();
       K *dst = static_cast<K *>(ws.keys[f.parity ^ 1]);
