@@ -395,6 +395,8 @@ def dist_sort(keys, values=None, *, width: int, key_kind: int = _lib.BS_KEY_UNSI
         k, v = ops.sort(keys, values)
         return DistResult(k, v, [keys.numel()], [keys.numel()])
     dev = keys.device
+    if exchange == "peer":
+        return _dist_sort_peer(keys, values, ops, group, R, rank, samples_per_rank)
     # 1. splitters from gathered samples
     smp = ops.sample(keys, samples_per_rank if keys.numel() else 0)
     cnt = torch.tensor([smp.numel()], dtype=torch.int64, device=dev)
@@ -409,23 +411,6 @@ def dist_sort(keys, values=None, *, width: int, key_kind: int = _lib.BS_KEY_UNSI
     ssorted = ops.sort_samples(allsmp)
     spl_host = choose_splitters(_to_unsigned_np(ssorted), R)
     splitters = torch.from_numpy(spl_host.view(_np_signed(keys.element_size()))).to(dev)
-    if exchange == "peer":
-        # 2+3. class counts of every shard (the host read also orders this
-        # rank's previous local sort -- which reads its receive buffer --
-        # before the all-gather, so no peer overwrites a buffer still in use)
-        cc = _all_gather_np(ops.split_count(keys, splitters, R).cpu().numpy(), group, dev).astype(np.int64)
-        B, delta, rcounts = exchange_plan(cc, R, rank)
-        kb = keys.element_size()
-        vb = values.element_size() if values is not None else 0
-        bufs = _peer_buffers(group, dev).ensure(int(rcounts.max()), kb, vb)
-        # 4. fused partition + peer stores, then every rank's stores land
-        ops.exchange(keys, values, splitters, R, delta, B, bufs)
-        _barrier(group, dev)
-        # 5. local sort out of the receive buffer
-        out_k, out_v = ops.sort_from(bufs, int(rcounts[rank]), keys.dtype,
-                                     values.dtype if values is not None else None)
-        scounts = send_counts(cc, B, rank)
-        return DistResult(out_k, out_v, scounts, [send_counts(cc, B, src)[rank] for src in range(R)])
     # 2. destination partition
     send_k, send_v, class_counts = ops.split(keys, values, splitters, R)
     # 3. count exchange + tie division
@@ -445,6 +430,51 @@ def dist_sort(keys, values=None, *, width: int, key_kind: int = _lib.BS_KEY_UNSI
     # 5. local (stable) sort; sources arrive in rank order
     recv_k, recv_v = ops.sort(recv_k, recv_v)
     return DistResult(recv_k, recv_v, scounts, rcounts)
+
+
+def _all_gather_dev(t, group):
+    """All-gather a small device tensor -> [R, *t.shape] on the same device (one collective)."""
+    import torch
+    import torch.distributed as dist
+
+    R = _world(group)
+    if _on_device(group):
+        out = torch.empty((R,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        dist.all_gather_into_tensor(out, t.contiguous(), group=group)
+        return out
+    parts = [torch.empty_like(t) for _ in range(R)]
+    dist.all_gather(parts, t.contiguous(), group=group)
+    return torch.stack(parts)
+
+
+def _dist_sort_peer(keys, values, ops, group, R: int, rank: int, S: int) -> DistResult:
+    """dist_sort with the fused partition + peer-store exchange (one host sync per call)."""
+    import torch
+
+    dev = keys.device
+    # 1. splitters on the device: S normalised samples per rank (an empty shard
+    # contributes the maximum word), all-gathered, sorted, quantiles i*S
+    if keys.numel():
+        smp = ops.sample(keys, S)
+    else:
+        smp = torch.full((S,), -1, dtype=keys.dtype, device=dev)
+    ssorted = ops.sort_samples(_all_gather_dev(smp, group).reshape(-1))
+    splitters = ssorted[torch.arange(1, R, device=dev) * S].contiguous()  # == choose_splitters
+    # 2+3. class counts of every shard; the one host read also orders this
+    # rank's previous local sort (which reads its receive buffer) before the
+    # all-gather completes anywhere, so no peer overwrites a buffer in use
+    cc = _all_gather_dev(ops.split_count(keys, splitters, R), group).cpu().numpy().astype(np.int64)
+    B, delta, rcounts = exchange_plan(cc, R, rank)
+    kb = keys.element_size()
+    vb = values.element_size() if values is not None else 0
+    bufs = _peer_buffers(group, dev).ensure(int(rcounts.max()), kb, vb)
+    # 4. fused partition + peer stores, then every rank's stores land
+    ops.exchange(keys, values, splitters, R, delta, B, bufs)
+    _barrier(group, dev)
+    # 5. local sort out of the receive buffer
+    out_k, out_v = ops.sort_from(bufs, int(rcounts[rank]), keys.dtype, values.dtype if values is not None else None)
+    scounts = send_counts(cc, B, rank)
+    return DistResult(out_k, out_v, scounts, [send_counts(cc, B, src)[rank] for src in range(R)])
 
 
 def _np_signed(itemsize: int):
