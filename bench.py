@@ -390,6 +390,8 @@ def run_gpu(args):
             line["e2e"] = e2e(args, host, dev)
         if not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args.cpu_sample)
+    if world > 1 and not args.no_e2e:
+        line["e2e"] = e2e_dist(args, host, dev, world, share)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -397,6 +399,43 @@ def run_gpu(args):
 
         dist.destroy_process_group()
     return 0
+
+
+def e2e_dist(args, host: np.ndarray, dev, world: int, share: bool):
+    """N>1 end to end through the public multi-GPU API: every rank copies its
+    shard from pinned host memory, runs dist_sort, and reads its slice of the
+    global order back into pinned host memory; max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_0811_3448_b200.dist import dist_sort
+
+    n = host.size
+    pinned_src = torch.from_numpy(host.view(np.int32)).pin_memory()
+    pinned_out = torch.empty(2 * n + 4096, dtype=torch.int32).pin_memory()  # a slice is ~n keys
+    times, nout = [], 0
+    steps = max(1, min(args.steps, args.e2e_steps))
+    for i in range(1 + steps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        keys = pinned_src.to(dev, non_blocking=True)
+        r = dist_sort(keys, width=32)
+        out = pinned_out[:r.keys.numel()] if r.keys.numel() <= pinned_out.numel() else \
+            torch.empty(r.keys.numel(), dtype=r.keys.dtype).pin_memory()
+        out.copy_(r.keys, non_blocking=True)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        nout = r.keys.numel()
+        if i > 0:
+            times.append(dt)
+    ms = torch.tensor([1e3 * sum(times) / len(times)], dtype=torch.float64, device="cpu" if share else dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    return {"value": n * world / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 4 * n,
+            "d2h_bytes_per_step": 4 * nout, "ms_per_step": ms, "steps": len(times),
+            "api": "paper_0811_3448_b200.dist.dist_sort(shard copied from pinned host memory) + D2H of the slice",
+            "per_rank_bytes": True}
 
 
 def e2e(args, host: np.ndarray, dev):
