@@ -57,16 +57,25 @@ static cudaError_t pdl_launch(void (*kern)(KArgs...), int grid, int block, size_
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+// Per-device one-time setup (function attributes, grid sizes) is keyed by the
+// current device, so one process may sort on several GPUs.
+constexpr int MAX_DEV = 64;
+
+static int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev >= 0 && dev < MAX_DEV ? dev : 0;
+}
+
 static int num_sms() {
-  static int sms = 0;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
+  static int sms[MAX_DEV] = {};
+  static std::once_flag once[MAX_DEV];
+  const int dev = current_device();
+  std::call_once(once[dev], [dev] {
+    cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+    if (sms[dev] <= 0) sms[dev] = 148;
   });
-  return sms;
+  return sms[dev];
 }
 
 // ----- tuning (per record width) --------------------------------------------
@@ -225,10 +234,17 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   constexpr int H16_BLOCK = 1024;
   constexpr size_t H16_SMEM = 32768 * sizeof(uint32_t);
   auto h16 = hist16_kernel<K, KIND, H16_BLOCK>;
-  static int sc_grid = 0, lc_grid = 0, hk_grid = 0, dk_grid = 0, db_grid = 0;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] {
+  struct Setup {
+    int sc_grid, lc_grid, hk_grid, dk_grid, db_grid;
+    cudaError_t attr_err;
+  };
+  static Setup setup[MAX_DEV];
+  static std::once_flag once[MAX_DEV];
+  const int dev = current_device();
+  int &sc_grid = setup[dev].sc_grid, &lc_grid = setup[dev].lc_grid, &hk_grid = setup[dev].hk_grid,
+      &dk_grid = setup[dev].dk_grid, &db_grid = setup[dev].db_grid;
+  cudaError_t &attr_err = setup[dev].attr_err;
+  std::call_once(once[dev], [&] {
     cudaError_t e1 = cudaFuncSetAttribute(sc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SS::bytes));
     cudaError_t e2 = cudaFuncSetAttribute(lc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(LS::bytes));
     cudaError_t e3 = cudaFuncSetAttribute(sw, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SW::bytes));
