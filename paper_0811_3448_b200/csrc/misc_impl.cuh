@@ -224,22 +224,111 @@ constexpr int SPLIT_BLOCK = 256;
 constexpr int SPLIT_KPT = 16;
 constexpr int SPLIT_TILE = SPLIT_BLOCK * SPLIT_KPT;
 
+// R <= 8 ranks: at most 7 splitters, held in registers (no shared loads per key)
+constexpr int SPLIT_MAXSP = 7;
+
+// Class of a normalised key against the (<= 7, sorted) splitters held in
+// shared memory padded to 8 with the maximum word: branchless lower bound
+// (3 probes) for #{s_j < key}, then one probe for "equals a splitter".
+// Same classes as split_class().
+template <typename K>
+struct SplitClass {
+  const K *s;  // shared, 8 entries
+  int nsp;
+  __device__ __forceinline__ uint32_t cls(K nk) const {
+    uint32_t lt = 0;
+#pragma unroll
+    for (uint32_t step = 4; step > 0; step >>= 1)
+      if (s[lt + step - 1] < nk) lt += step;
+    const uint32_t eq = (int(lt) < nsp && s[lt] == nk) ? 1u : 0u;
+    return 2u * lt + eq;
+  }
+};
+
+template <typename K>
+__device__ __forceinline__ void load_splitters(K *s_spl, const K *spl, int nsp) {
+  if (threadIdx.x < SPLIT_MAXSP + 1) s_spl[threadIdx.x] = int(threadIdx.x) < nsp ? spl[threadIdx.x] : ~K(0);
+}
+
+// Fast path: a 256-entry table on the key's top byte.  Entry t holds the
+// class of every key whose top byte is t when no splitter lies in that byte
+// range (all but <= 7 entries), else 0xFF (take the binary search).
+template <typename K>
+struct SplitLUT {
+  const uint8_t *tab;  // shared, 256 entries
+  SplitClass<K> sc;
+  __device__ __forceinline__ uint32_t cls(K nk) const {
+    constexpr int W = int(sizeof(K)) * 8;
+    const uint32_t c = tab[uint32_t(nk >> (W - 8))];
+    return c != 0xFFu ? c : sc.cls(nk);
+  }
+};
+
+// build the table (call with >= 256 threads after the splitters are in shared memory + a barrier)
+template <typename K>
+__device__ __forceinline__ void build_split_lut(uint8_t *tab, const SplitClass<K> &sc) {
+  constexpr int W = int(sizeof(K)) * 8;
+  const uint32_t t = threadIdx.x;
+  if (t < 256) {
+    const K lo = K(t) << (W - 8), hi = lo | (~K(0) >> 8);
+    const uint32_t a = sc.cls(lo), b = sc.cls(hi);
+    tab[t] = (a == b && (a & 1u) == 0u) ? uint8_t(a) : uint8_t(0xFF);
+  }
+}
+
+// Per-tile class counts.  Each thread counts its 16 keys in packed 8-bit
+// fields (classes 0-7 / 8-15 in two 64-bit words), the warp sums 16-bit
+// fields with shuffles, and one shared atomic per class and warp folds the
+// warps: no same-address shared atomics per key (16 classes would serialise).
 template <typename K, int KIND>
-__global__ void split_hist_kernel(const K *keys, uint64_t n, int shift0, const K *spl, int nsp,
-                                  uint32_t *tile_hist /* [ntiles][16] */) {
+__global__ void __launch_bounds__(SPLIT_BLOCK) split_hist_kernel(const K *keys, uint64_t n, int shift0,
+                                                                 const K *spl, int nsp,
+                                                                 uint32_t *tile_hist /* [ntiles][16] */) {
   const KeyGeom<K, KIND> g{shift0};
   __shared__ uint32_t h[16];
-  __shared__ K s_spl[16];
-  if (threadIdx.x < 16) h[threadIdx.x] = 0;
-  if (threadIdx.x < nsp) s_spl[threadIdx.x] = spl[threadIdx.x];
+  __shared__ K s_spl[SPLIT_MAXSP + 1];
+  __shared__ uint8_t s_tab[256];
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid < 16) h[tid] = 0;
+  load_splitters(s_spl, spl, nsp);
+  const SplitClass<K> sc{s_spl, nsp};
+  __syncthreads();
+  build_split_lut(s_tab, sc);
+  const SplitLUT<K> sr{s_tab, sc};
   __syncthreads();
   const uint64_t base = uint64_t(blockIdx.x) * SPLIT_TILE;
+  const int cnt = int(min64(SPLIT_TILE, n - base));
+  // all loads first (no per-key branch between them), then classify
+  K x[SPLIT_KPT];
+#pragma unroll
   for (int j = 0; j < SPLIT_KPT; ++j) {
-    const uint64_t i = base + uint64_t(j) * SPLIT_BLOCK + threadIdx.x;
-    if (i < n) atomicAdd(&h[split_class(g.norm(keys[i]), s_spl, nsp)], 1u);
+    const int e = j * SPLIT_BLOCK + tid;
+    x[j] = e < cnt ? keys[base + e] : K(0);
+  }
+  uint64_t lo = 0, hi = 0;
+#pragma unroll
+  for (int j = 0; j < SPLIT_KPT; ++j) {
+    const uint32_t c = sr.cls(g.norm(x[j]));
+    const uint64_t inc = (j * SPLIT_BLOCK + tid < cnt) ? (1ull << (8 * (c & 7u))) : 0ull;
+    if (c < 8u) lo += inc;
+    else hi += inc;
+  }
+  // widen to 16-bit fields (a warp holds up to 32*16 = 512 per class)
+  uint64_t f[4] = {lo & 0x00FF00FF00FF00FFull, (lo >> 8) & 0x00FF00FF00FF00FFull, hi & 0x00FF00FF00FF00FFull,
+                   (hi >> 8) & 0x00FF00FF00FF00FFull};
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) f[q] += __shfl_xor_sync(0xFFFFFFFFu, f[q], o);
+  if (lane < 16) {  // lane c reports class c
+    // f[0]: classes 0,2,4,6  f[1]: 1,3,5,7  f[2]: 8,10,12,14  f[3]: 9,11,13,15
+    const int c = lane;
+    const uint64_t word = (c >> 3) ? ((c & 1) ? f[3] : f[2]) : ((c & 1) ? f[1] : f[0]);
+    const uint32_t v = uint32_t(word >> (16 * ((c & 7) >> 1))) & 0xFFFFu;
+    if (v) atomicAdd(&h[c], v);
   }
   __syncthreads();
-  if (threadIdx.x < 16) tile_hist[size_t(blockIdx.x) * 16 + threadIdx.x] = h[threadIdx.x];
+  if (tid < 16) tile_hist[size_t(blockIdx.x) * 16 + tid] = h[tid];
 }
 
 template <typename K, int VB, int KIND>
@@ -475,27 +564,26 @@ __global__ void __launch_bounds__(SPLIT_BLOCK) split_exchange_kernel(
   V *vstage = reinterpret_cast<V *>(xsm + S::vals_off);
   __shared__ uint32_t wrun[NW][16];
   __shared__ uint32_t tb[17];
-  __shared__ uint32_t s_off[16];
-  __shared__ long long s_delta[16];
+  __shared__ long long s_g[16];  // global position of tile position i in class c: s_g[c] + i
   __shared__ unsigned long long s_bnd[9];
-  __shared__ K s_spl[16];
   __shared__ K *s_dk[8];
   __shared__ V *s_dv[8];
   const KeyGeom<K, KIND> g{shift0};
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int ncls = 2 * nsp + 1;
-  if (tid < nsp) s_spl[tid] = spl[tid];
-  if (tid < 16) {
-    s_off[tid] = tile_off[size_t(blockIdx.x) * 16 + tid];
-    s_delta[tid] = tid < ncls ? delta[tid] : 0;
-    wrun[0][tid] = 0;
-  }
-  if (tid < NW * 16 && tid >= 16) (&wrun[0][0])[tid] = 0;
+  __shared__ K s_spl[SPLIT_MAXSP + 1];
+  __shared__ uint8_t s_tab[256];
+  load_splitters(s_spl, spl, nsp);
+  const SplitClass<K> sc{s_spl, nsp};
+  for (int i = tid; i < NW * 16; i += SPLIT_BLOCK) (&wrun[0][0])[i] = 0;
   if (tid <= nranks) s_bnd[tid] = bounds[tid];
   if (tid < nranks) {
     s_dk[tid] = dst_keys[tid];
     if constexpr (VB != 0) s_dv[tid] = static_cast<V *>(dst_vals[tid]);
   }
+  __syncthreads();
+  build_split_lut(s_tab, sc);
+  const SplitLUT<K> sr{s_tab, sc};
   __syncthreads();
   const V *vals = static_cast<const V *>(vals_);
   const uint64_t base = uint64_t(blockIdx.x) * SPLIT_TILE;
@@ -505,25 +593,38 @@ __global__ void __launch_bounds__(SPLIT_BLOCK) split_exchange_kernel(
   K x[SPLIT_KPT];
   V v[SPLIT_KPT];
   uint32_t dr[SPLIT_KPT];  // class | rank-in-warp << 8
+  // all loads first (the ranking below is warp-collective, so loads inside
+  // it would wait one by one)
+#pragma unroll
+  for (int j = 0; j < SPLIT_KPT; ++j) {
+    const int e = wbase + 32 * j + lane;
+    x[j] = K(0);
+    if (e < cnt) {
+      x[j] = keys[base + e];
+      if constexpr (VB != 0) v[j] = vals[base + e];
+    }
+  }
 #pragma unroll
   for (int j = 0; j < SPLIT_KPT; ++j) {
     const int e = wbase + 32 * j + lane;
     const bool valid = e < cnt;
-    uint32_t d = 0xFFu;
-    if (valid) {
-      x[j] = keys[base + e];
-      if constexpr (VB != 0) v[j] = vals[base + e];
-      d = split_class(g.norm(x[j]), s_spl, nsp);
+    const uint32_t d = valid ? sr.cls(g.norm(x[j])) : 0u;
+    // stable rank among this warp's elements of the same class (element
+    // order j-major, lane-minor): 4 ballots match the class's 4 bits
+    uint32_t peers = __ballot_sync(0xFFFFFFFFu, valid);
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const bool bit = (d >> b) & 1u;
+      const uint32_t bb = __ballot_sync(0xFFFFFFFFu, bit);
+      peers &= bit ? bb : ~bb;
     }
-    // stable rank among this warp's elements of the same class (element order j-major, lane-minor)
-    const uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
     const uint32_t below = __popc(peers & lt);
     uint32_t old = 0;
     if (valid && below == 0) {
       old = wrun[w][d];
       wrun[w][d] = old + __popc(peers);
     }
-    old = __shfl_sync(0xFFFFFFFFu, old, __ffs(peers) - 1);
+    old = __shfl_sync(0xFFFFFFFFu, old, valid ? __ffs(peers) - 1 : lane);
     dr[j] = d | ((old + below) << 8);
     __syncwarp();
   }
@@ -543,6 +644,9 @@ __global__ void __launch_bounds__(SPLIT_BLOCK) split_exchange_kernel(
     for (int c = 1; c <= 16; ++c) tb[c] += tb[c - 1];
   }
   __syncthreads();
+  if (tid < 16)  // shard class-major position -> global position
+    s_g[tid] = (long long)tile_off[size_t(blockIdx.x) * 16 + tid] + (tid < ncls ? delta[tid] : 0) -
+               (long long)tb[tid];
 #pragma unroll
   for (int j = 0; j < SPLIT_KPT; ++j) {
     const int e = wbase + 32 * j + lane;
@@ -554,19 +658,56 @@ __global__ void __launch_bounds__(SPLIT_BLOCK) split_exchange_kernel(
     }
   }
   __syncthreads();
-  for (int i = tid; i < cnt; i += SPLIT_BLOCK) {
-    int c = 0;
-#pragma unroll
-    for (int k = 1; k < 16; ++k) c += (uint32_t(i) >= tb[k]) ? 1 : 0;
-    const uint64_t gpos = uint64_t(int64_t(s_off[c] + (uint32_t(i) - tb[c])) + s_delta[c]);
-    int d = 0;
-    for (int k = 1; k < nranks; ++k) d += (gpos >= s_bnd[k]) ? 1 : 0;
-    const uint64_t o = gpos - s_bnd[d];
-    s_dk[d][o] = stage[i];
-    if constexpr (VB != 0) s_dv[d][o] = vstage[i];
+  // Write-out by segments: the tile's positions, in class order, map to
+  // increasing global positions; cutting them at class starts and at the
+  // destination boundaries gives <= 15 + 7 segments, each a contiguous run
+  // with one destination and one offset.  One thread lists the segments,
+  // then each warp stores 32 consecutive positions per step.
+  __shared__ uint32_t seg_start[24];
+  __shared__ long long seg_off[24];
+  __shared__ uint32_t seg_dst[24];
+  if (tid == 0) {
+    int k = 0;
+    for (int c = 0; c < 16; ++c) {
+      const uint32_t a0 = tb[c], b0 = tb[c + 1];
+      for (uint32_t i = a0; i < b0;) {
+        const unsigned long long gpos = (unsigned long long)(s_g[c] + (long long)i);
+        int d = 0;
+        while (d + 1 < nranks && gpos >= s_bnd[d + 1]) ++d;
+        uint32_t iend = b0;
+        if (d + 1 < nranks) {
+          const unsigned long long lim = s_bnd[d + 1] - (unsigned long long)s_g[c];
+          if (lim < iend) iend = uint32_t(lim);
+        }
+        seg_start[k] = i;
+        seg_off[k] = s_g[c] - (long long)s_bnd[d];
+        seg_dst[k] = uint32_t(d);
+        ++k;
+        i = iend;
+      }
+    }
+    seg_start[k] = uint32_t(cnt);  // sentinel
   }
-  // the stores must be visible to the receiving GPUs once this grid is done
-  __threadfence_system();
+  __syncthreads();
+  int si = 0;
+  for (int base_i = w * 32; base_i < cnt; base_i += SPLIT_BLOCK) {
+    while (seg_start[si + 1] <= uint32_t(base_i)) ++si;  // warp-uniform
+    const int i = base_i + lane;
+    if (i < cnt) {
+      int sj = si;
+      while (seg_start[sj + 1] <= uint32_t(i)) ++sj;  // a chunk crossing a segment end
+      const uint64_t o = uint64_t((long long)i + seg_off[sj]);
+      s_dk[seg_dst[sj]][o] = stage[i];
+      if constexpr (VB != 0) s_dv[seg_dst[sj]][o] = vstage[i];
+    }
+  }
+  // The receivers are ordered after this grid by stream order on this GPU
+  // plus a collective (its system-scope release comes later in the stream).
+  // One system fence per CTA, after all of the CTA's stores (cumulative
+  // through the barrier), keeps the ordering explicit without making every
+  // thread wait for its own stores to drain.
+  __syncthreads();
+  if (tid == 0) __threadfence_system();
 }
 
 }  // namespace bs
