@@ -552,7 +552,7 @@ struct ExchangeSmem {
 };
 
 template <typename K, int VB, int KIND>
-__global__ void __launch_bounds__(SPLIT_BLOCK) split_exchange_kernel(
+__global__ void __launch_bounds__(SPLIT_BLOCK, sizeof(K) + VB <= 4 ? 4 : sizeof(K) + VB <= 8 ? 3 : 2) split_exchange_kernel(
     const K *keys, const void *vals_, uint64_t n, int shift0, const K *spl, int nsp, const uint32_t *tile_off,
     const long long *delta, const unsigned long long *bounds, int nranks, K *const *dst_keys,
     void *const *dst_vals) {
