@@ -621,7 +621,8 @@ static int split_count(const void *keys, uint64_t n, int key_bytes, int width, i
   return split_dispatch(key_bytes, key_kind, 0, [&](auto ktag, auto kindc, auto) -> int {
     using K = decltype(ktag);
     constexpr int KIND = decltype(kindc)::value;
-    split_hist_kernel<K, KIND><<<w.ntiles, SPLIT_BLOCK, 0, st>>>(static_cast<const K *>(keys), n, shift0,
+    split_hist_kernel<K, KIND><<<(w.ntiles + SPLIT_HIST_TPB - 1) / SPLIT_HIST_TPB, SPLIT_BLOCK, 0, st>>>(
+        static_cast<const K *>(keys), n, shift0,
                                                                  static_cast<const K *>(splitters), nsp, w.tile_hist);
     split_chunk_sum_kernel<<<w.nchunks, 256, 0, st>>>(w.tile_hist, w.ntiles, w.chunk_sum);
     split_top_scan_kernel<<<1, 512, 0, st>>>(w.chunk_sum, w.nchunks, ncls,

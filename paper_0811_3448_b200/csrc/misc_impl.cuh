@@ -226,6 +226,7 @@ constexpr int SPLIT_TILE = SPLIT_BLOCK * SPLIT_KPT;
 
 // R <= 8 ranks: at most 7 splitters, held in registers (no shared loads per key)
 constexpr int SPLIT_MAXSP = 7;
+constexpr int SPLIT_HIST_TPB = 4;  // tiles per split_hist_kernel CTA
 
 // Class of a normalised key against the (<= 7, sorted) splitters held in
 // shared memory padded to 8 with the maximum word: branchless lower bound
@@ -296,39 +297,48 @@ __global__ void __launch_bounds__(SPLIT_BLOCK) split_hist_kernel(const K *keys, 
   build_split_lut(s_tab, sc);
   const SplitLUT<K> sr{s_tab, sc};
   __syncthreads();
-  const uint64_t base = uint64_t(blockIdx.x) * SPLIT_TILE;
-  const int cnt = int(min64(SPLIT_TILE, n - base));
-  // all loads first (no per-key branch between them), then classify
-  K x[SPLIT_KPT];
+  // SPLIT_HIST_TPB consecutive tiles per CTA (the table build is amortised)
+  const uint64_t ntiles = (n + SPLIT_TILE - 1) / SPLIT_TILE;
+  for (uint64_t t = uint64_t(blockIdx.x) * SPLIT_HIST_TPB;
+       t < min64(ntiles, uint64_t(blockIdx.x + 1) * SPLIT_HIST_TPB); ++t) {
+    const uint64_t base = t * SPLIT_TILE;
+    const int cnt = int(min64(SPLIT_TILE, n - base));
+    // all loads first (no per-key branch between them), then classify
+    K x[SPLIT_KPT];
 #pragma unroll
-  for (int j = 0; j < SPLIT_KPT; ++j) {
-    const int e = j * SPLIT_BLOCK + tid;
-    x[j] = e < cnt ? keys[base + e] : K(0);
+    for (int j = 0; j < SPLIT_KPT; ++j) {
+      const int e = j * SPLIT_BLOCK + tid;
+      x[j] = e < cnt ? keys[base + e] : K(0);
+    }
+    uint64_t lo = 0, hi = 0;
+#pragma unroll
+    for (int j = 0; j < SPLIT_KPT; ++j) {
+      const uint32_t c = sr.cls(g.norm(x[j]));
+      const uint64_t inc = (j * SPLIT_BLOCK + tid < cnt) ? (1ull << (8 * (c & 7u))) : 0ull;
+      if (c < 8u) lo += inc;
+      else hi += inc;
+    }
+    // widen to 16-bit fields (a warp holds up to 32*16 = 512 per class)
+    uint64_t f[4] = {lo & 0x00FF00FF00FF00FFull, (lo >> 8) & 0x00FF00FF00FF00FFull, hi & 0x00FF00FF00FF00FFull,
+                     (hi >> 8) & 0x00FF00FF00FF00FFull};
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) f[q] += __shfl_xor_sync(0xFFFFFFFFu, f[q], o);
+    if (lane < 16) {  // lane c reports class c
+      // f[0]: classes 0,2,4,6  f[1]: 1,3,5,7  f[2]: 8,10,12,14  f[3]: 9,11,13,15
+      const int c = lane;
+      const uint64_t word = (c >> 3) ? ((c & 1) ? f[3] : f[2]) : ((c & 1) ? f[1] : f[0]);
+      const uint32_t v = uint32_t(word >> (16 * ((c & 7) >> 1))) & 0xFFFFu;
+      if (v) atomicAdd(&h[c], v);
+    }
+    __syncthreads();
+    if (tid < 16) {
+      tile_hist[size_t(t) * 16 + tid] = h[tid];
+      h[tid] = 0;
+    }
+    __syncthreads();
   }
-  uint64_t lo = 0, hi = 0;
-#pragma unroll
-  for (int j = 0; j < SPLIT_KPT; ++j) {
-    const uint32_t c = sr.cls(g.norm(x[j]));
-    const uint64_t inc = (j * SPLIT_BLOCK + tid < cnt) ? (1ull << (8 * (c & 7u))) : 0ull;
-    if (c < 8u) lo += inc;
-    else hi += inc;
-  }
-  // widen to 16-bit fields (a warp holds up to 32*16 = 512 per class)
-  uint64_t f[4] = {lo & 0x00FF00FF00FF00FFull, (lo >> 8) & 0x00FF00FF00FF00FFull, hi & 0x00FF00FF00FF00FFull,
-                   (hi >> 8) & 0x00FF00FF00FF00FFull};
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) f[q] += __shfl_xor_sync(0xFFFFFFFFu, f[q], o);
-  if (lane < 16) {  // lane c reports class c
-    // f[0]: classes 0,2,4,6  f[1]: 1,3,5,7  f[2]: 8,10,12,14  f[3]: 9,11,13,15
-    const int c = lane;
-    const uint64_t word = (c >> 3) ? ((c & 1) ? f[3] : f[2]) : ((c & 1) ? f[1] : f[0]);
-    const uint32_t v = uint32_t(word >> (16 * ((c & 7) >> 1))) & 0xFFFFu;
-    if (v) atomicAdd(&h[c], v);
-  }
-  __syncthreads();
-  if (tid < 16) tile_hist[size_t(blockIdx.x) * 16 + tid] = h[tid];
 }
 
 template <typename K, int VB, int KIND>
