@@ -614,6 +614,18 @@ __global__ void __launch_bounds__(SPLIT_BLOCK, sizeof(K) + VB <= 4 ? 4 : sizeof(
       if constexpr (VB != 0) v[j] = vals[base + e];
     }
   }
+  if constexpr (VB == 0) {
+    // keys only: order inside a class is immaterial (the receiver sorts) --
+    // the rank is the arrival slot on the warp's own class counter
+#pragma unroll
+    for (int j = 0; j < SPLIT_KPT; ++j) {
+      const int e = wbase + 32 * j + lane;
+      if (e < cnt) {
+        const uint32_t d = sr.cls(g.norm(x[j]));
+        dr[j] = d | (atomicAdd(&wrun[w][d], 1u) << 8);
+      }
+    }
+  } else
 #pragma unroll
   for (int j = 0; j < SPLIT_KPT; ++j) {
     const int e = wbase + 32 * j + lane;
