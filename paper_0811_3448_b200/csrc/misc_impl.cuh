@@ -715,9 +715,16 @@ __global__ void __launch_bounds__(SPLIT_BLOCK, sizeof(K) + VB <= 4 ? 4 : sizeof(
   for (int base_i = w * 32; base_i < cnt; base_i += SPLIT_BLOCK) {
     while (seg_start[si + 1] <= uint32_t(base_i)) ++si;  // warp-uniform
     const int i = base_i + lane;
-    if (i < cnt) {
+    if (seg_start[si + 1] >= uint32_t(min(base_i + 32, cnt))) {  // whole chunk in one segment (usual)
+      const long long off = seg_off[si];
+      const uint32_t dd = seg_dst[si];
+      if (i < cnt) {
+        s_dk[dd][i + off] = stage[i];
+        if constexpr (VB != 0) s_dv[dd][i + off] = vstage[i];
+      }
+    } else if (i < cnt) {
       int sj = si;
-      while (seg_start[sj + 1] <= uint32_t(i)) ++sj;  // a chunk crossing a segment end
+      while (seg_start[sj + 1] <= uint32_t(i)) ++sj;  // the chunk crosses a segment end
       const uint64_t o = uint64_t((long long)i + seg_off[sj]);
       s_dk[seg_dst[sj]][o] = stage[i];
       if constexpr (VB != 0) s_dv[seg_dst[sj]][o] = vstage[i];
