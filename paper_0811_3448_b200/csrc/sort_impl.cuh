@@ -1715,30 +1715,28 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
         const uint32_t nbins = 1u << B, bmask = nbins - 1u;
         uint32_t *bins = whist_all;
         for (uint32_t i = tid; i < nbins; i += BLOCK) bins[i] = 0;
+        if (tid == 0) misc[48] = 0;
         __syncthreads();
+        // comparisons a plain in-bin ranking needs: sum over bins of c^2 =
+        // sum over keys of (2 * arrival slot + 1) -- no pass over the bins
         Ranks<KPT> slot;  // arrival slot inside the bin
         slot.clear();
+        uint32_t c2 = 0;
 #pragma unroll
         for (int j = 0; j < KPT; ++j) {
           if (j >= kk) break;
-          if (32 * j + lane < nvw) slot.set(j, atomicAdd(&bins[uint32_t(g.norm(x[j]) >> sh) & bmask], 1u));
+          if (32 * j + lane < nvw) {
+            const uint32_t sl = atomicAdd(&bins[uint32_t(g.norm(x[j]) >> sh) & bmask], 1u);
+            slot.set(j, sl);
+            c2 += 2u * sl + 1u;
+          }
         }
+        c2 = __reduce_add_sync(0xFFFFFFFFu, c2);
+        if (lane == 0 && c2) atomicAdd(&misc[48], c2);
         __syncthreads();
         const uint32_t bpt = (nbins + BLOCK - 1) / BLOCK;
         const uint32_t q0 = min(nbins, uint32_t(tid) * bpt), q1 = min(nbins, q0 + bpt);
         const bool vec = (bpt & 3u) == 0u;  // whole uint4 chunks (conflict-free scan loads)
-        // comparisons a plain in-bin ranking needs: sum of c^2 over all bins
-        if (tid == 0) misc[48] = 0;
-        {
-          uint32_t c2 = 0;
-          for (uint32_t q = tid; q < nbins; q += BLOCK) {  // strided: conflict-free
-            const uint32_t v = bins[q];
-            c2 += v * v;
-          }
-          __syncthreads();
-          c2 = __reduce_add_sync(0xFFFFFFFFu, c2);
-          if (lane == 0 && c2) atomicAdd(&misc[48], c2);
-        }
         {
           uint4 *b4 = reinterpret_cast<uint4 *>(bins);
           uint32_t c = 0;
