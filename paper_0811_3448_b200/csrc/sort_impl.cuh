@@ -1067,7 +1067,7 @@ struct ScatterSmem {
 };
 
 template <typename K, int VB, int KIND, int BLOCK, int KPT>
-__global__ void __launch_bounds__(BLOCK) scatter_kernel(Ws ws, int L) {
+__global__ void __launch_bounds__(BLOCK, (sizeof(K) + VB) <= 8 ? 3 : 1) scatter_kernel(Ws ws, int L) {
   pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
   using S = ScatterSmem<K, VB, KIND, BLOCK, KPT>;
   using D = typename S::D;
