@@ -294,6 +294,20 @@ def test_kv_u64_keys_u64_values(cuda):
     assert np.array_equal(kk, k[order]) and np.array_equal(vv, v[order])
 
 
+@pytest.mark.parametrize("kdt,vdt", [(np.uint32, np.uint64), (np.uint64, np.uint32), (np.uint32, np.uint32)])
+def test_kv_mixed_widths_stable(cuda, kdt, vdt):
+    # several scatter levels (tiles of the stable scatter + tile scan) and ties
+    rng = np.random.default_rng(14)
+    n = (1 << 22) + 12345
+    bits = 8 * np.dtype(kdt).itemsize
+    k = (rng.integers(0, 1 << 20, n, dtype=np.uint64) << np.uint64(bits - 20)).astype(kdt)
+    v = rng.integers(0, np.iinfo(vdt).max, n, dtype=np.uint64).astype(vdt)
+    kk, vv = k.copy(), v.copy()
+    bs.sort(kk, UnsignedCodec(bits), values=vv, with_metrics=False)
+    order = np.argsort(k, kind="stable")
+    assert np.array_equal(kk, k[order]) and np.array_equal(vv, v[order])
+
+
 def test_variants_same_output(cuda):
     rng = np.random.default_rng(40)
     base = rng.integers(0, 2 ** 32, 200000, dtype=np.uint64).astype(np.uint32)
