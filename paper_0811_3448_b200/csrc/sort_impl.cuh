@@ -1714,7 +1714,7 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
         const int sh = hb + 1 - B;
         const uint32_t nbins = 1u << B, bmask = nbins - 1u;
         uint32_t *bins = whist_all;
-        for (uint32_t i = tid; i < nbins; i += BLOCK) bins[i] = 0;
+        for (uint32_t i = tid; i < (nbins + 3) / 4; i += BLOCK) reinterpret_cast<uint4 *>(bins)[i] = make_uint4(0, 0, 0, 0);
         if (tid == 0) misc[48] = 0;
         __syncthreads();
         // comparisons a plain in-bin ranking needs: sum over bins of c^2 =
