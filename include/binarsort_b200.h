@@ -142,9 +142,11 @@ int bs_range_sorted(const void *keys, uint64_t n, int key_bytes, void *stream,
 
 /* ---------------------------------------------------------------------------
  * Multi-GPU front end (replaces variants.sort_parallel's serial top-bit
- * pre-partition + thread pool, variants.py:124-229).  The collective itself
- * (count exchange + all-to-all-v) is issued by the host over NCCL; these are
- * the per-rank device steps around it.
+ * pre-partition + thread pool, variants.py:124-229).  The host issues the
+ * small collectives (sample and class-count all-gathers) over NCCL; the data
+ * moves either through bs_split_exchange (fused partition + peer-memory
+ * stores, the product path) or through bs_split_by_splitters + an NCCL
+ * all-to-all-v (baseline).  These are the per-rank device steps.
  * ------------------------------------------------------------------------- */
 
 /*

@@ -1,4 +1,4 @@
-"""Multi-GPU front end: one process per GPU, range partition + one all-to-all-v.
+"""Multi-GPU front end: one process per GPU, range partition + a fused peer-memory exchange.
 
 Replaces the reference's bucket parallelism (``variants.sort_parallel``,
 ``variants.py:162-229``: a serial top-bit pre-partition on the main thread,
