@@ -209,3 +209,11 @@ def test_exchange_plan_matches_all_to_all(R, kind):
         keys_d = np.array([shards[i >> 32][i & 0xFFFFFFFF] for i in recv[dd]], dtype=np.uint32)
         keys_w = np.array([shards[i >> 32][i & 0xFFFFFFFF] for i in want], dtype=np.uint32)
         assert np.array_equal(recv[dd][np.argsort(keys_d, kind="stable")], want[np.argsort(keys_w, kind="stable")])
+
+
+@pytest.mark.parametrize("R,S", [(2, 4096), (3, 4096), (8, 4096), (8, 7)])
+def test_device_splitter_indices_match_choose_splitters(R, S):
+    """dist._dist_sort_peer picks sorted_samples[i*S] for i in 1..R-1 on the
+    device; that is choose_splitters() on the R*S gathered samples."""
+    s = np.arange(R * S, dtype=np.uint64) * np.uint64(3)
+    assert np.array_equal(choose_splitters(s, R), s[np.arange(1, R) * S])
