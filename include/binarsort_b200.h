@@ -57,6 +57,27 @@ const char *bs_last_error(void);
 size_t bs_workspace_bytes(uint64_t n, int key_bytes, int val_bytes);
 
 /*
+ * Device status of the last sort that used workspace `ws` (bs_sort or
+ * bs_sort_from): enqueues on `stream` a 4-byte copy of the sort's overflow
+ * flag into *status (device or pinned host memory).  0 = OK; otherwise bit 0
+ * bucket-list overflow, bit 1 tile-map overflow, bit 2 task-list overflow --
+ * work was dropped and the output is NOT sorted.  The capacities are sized so
+ * this cannot happen for any input (Geometry in binarsort_b200.cu); the flag
+ * is the loud failure path that proves it (the Python shim raises
+ * RuntimeError).  No reference counterpart: the numba kernels cannot run out
+ * of work-list space (kernels.py:88-126 recurses on the call stack).
+ */
+int bs_sort_status(const void *ws, int32_t *status, void *stream);
+
+/*
+ * Test hook: cap the work-list capacities (buckets, tiles, tasks) of the
+ * sorts this thread launches next; 0 = no cap.  Caps only shrink the lists, so
+ * any workspace sized by bs_workspace_bytes stays valid.  Used by the
+ * forced-overflow test to prove bs_sort_status reports dropped work.
+ */
+void bs_debug_capacity(uint32_t max_buckets, uint32_t max_tiles, uint32_t max_tasks);
+
+/*
  * Sort keys[0..n) (and vals[0..n) alongside, if vals != NULL) in place into
  * nondecreasing codec order.  Replaces kernels.sort_words(arr, lower, upper,
  * pos, width, False, 0, 0, False, counters, depth) (kernels.py:88-126) for the
@@ -179,6 +200,12 @@ int bs_split_by_splitters(const void *keys, const void *vals, uint64_t n,
  *     (bs_ipc_open).  Call with the same ws right after bs_split_count on the
  *     same keys.  The grid ends with a system-scope fence; the caller orders
  *     the receivers after it (stream order + a collective).
+ *     With vals the exchange is stable (class, then source rank, then shard
+ *     index).  Keys only, the order of elements within a class (and which
+ *     copies of a tie class land on which destination) is unspecified: they
+ *     are ranked by arrival on a shared counter, and the receiver's sort
+ *     orders them.  Keys tied on their low `width` bits may therefore arrive
+ *     in a run-dependent order.  nranks <= 8 (one NVSwitch node).
  * delta: device int64[2R-1]; bounds: device uint64[R+1].
  */
 int bs_split_count(const void *keys, uint64_t n, int key_bytes, int width,

@@ -35,6 +35,7 @@ EXPORTS = (
     "bs_split_by_splitters", "bs_sample_keys", "bs_sort_profiled", "bs_sort_launches",
     "bs_sort_from_workspace_bytes", "bs_sort_from", "bs_split_count", "bs_split_exchange",
     "bs_ipc_handle_bytes", "bs_ipc_alloc", "bs_ipc_open", "bs_ipc_close", "bs_ipc_free",
+    "bs_sort_status", "bs_debug_capacity",
 )
 
 
@@ -124,6 +125,10 @@ def lib() -> ctypes.CDLL:
         L.bs_ipc_close.restype = i32
         L.bs_ipc_free.argtypes = [vp]
         L.bs_ipc_free.restype = i32
+        L.bs_sort_status.argtypes = [vp, vp, vp]
+        L.bs_sort_status.restype = i32
+        L.bs_debug_capacity.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32]
+        L.bs_debug_capacity.restype = None
         _lib = L
         return L
 

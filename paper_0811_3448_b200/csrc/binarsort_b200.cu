@@ -104,6 +104,9 @@ struct Geometry {
   int ndig;
 };
 
+// bs_debug_capacity: thread-local caps on the work lists (0 = none)
+static thread_local uint32_t t_cap_b = 0, t_cap_t = 0, t_cap_k = 0;
+
 static Geometry geometry(uint64_t n, int kb, int vb, int width_eff) {
   Geometry g{};
   g.n = n;
@@ -170,8 +173,12 @@ template <typename K, int VB, int KIND>
 static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp, size_t ws_bytes,
                     cudaStream_t st, void *src_keys = nullptr, void *src_vals = nullptr) {
   const int kb = int(sizeof(K));
-  const Geometry geo = geometry(n, kb, VB, width_eff);
+  Geometry geo = geometry(n, kb, VB, width_eff);
   const Layout lay = layout(geo, src_keys == nullptr);
+  // test caps shrink the lists inside an unchanged layout (the flag reports it)
+  if (t_cap_b) geo.maxb = geo.maxb < t_cap_b ? geo.maxb : t_cap_b;
+  if (t_cap_t) geo.maxtiles = geo.maxtiles < t_cap_t ? geo.maxtiles : t_cap_t;
+  if (t_cap_k) geo.maxtasks = geo.maxtasks < t_cap_k ? geo.maxtasks : t_cap_k;
   if (ws_bytes < lay.total)
     return fail(BS_ERR_WORKSPACE, "workspace too small: need " + std::to_string(lay.total) +
                                       " bytes, got " + std::to_string(ws_bytes));
@@ -381,6 +388,20 @@ int bs_sort(void *keys, void *vals, uint64_t n, int key_bytes, int val_bytes, in
   if (rc) return rc;
   if (counters) return bs_metrics(keys, n, key_bytes, width, start_pos, key_kind, depth, nullptr, 0, stream, counters);
   return BS_OK;
+}
+
+int bs_sort_status(const void *ws, int32_t *status, void *stream) {
+  if (!ws || !status) return fail(BS_ERR_VALUE, "ws and status must be non-NULL");
+  // Ctl sits at offset 0 of every sort workspace (layout())
+  const char *flag = static_cast<const char *>(ws) + offsetof(Ctl, error);
+  BS_CUDA(cudaMemcpyAsync(status, flag, sizeof(int32_t), cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
+  return BS_OK;
+}
+
+void bs_debug_capacity(uint32_t max_buckets, uint32_t max_tiles, uint32_t max_tasks) {
+  t_cap_b = max_buckets;
+  t_cap_t = max_tiles;
+  t_cap_k = max_tasks;
 }
 
 size_t bs_sort_from_workspace_bytes(uint64_t n, int key_bytes, int val_bytes) {

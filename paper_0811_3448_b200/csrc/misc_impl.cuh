@@ -550,8 +550,14 @@ __global__ void __launch_bounds__(256) split_chunk_scan_kernel(uint32_t *tile_hi
 // so the element is stored straight into d's receive buffer at
 // gpos - bounds[d] -- a peer (NVLink / NVSwitch) store for d != this rank.
 // A tile is staged in shared memory in class order first, so consecutive
-// threads store consecutive addresses of each class run.  Stable: a class's
-// elements keep shard order, and ranks' blocks are in rank order (delta).
+// threads store consecutive addresses of each class run.  Key-value: stable
+// (a class's elements keep shard order -- stable ballot ranking -- and ranks'
+// blocks are in rank order via delta).  Keys only: within a class, elements
+// are ranked by their arrival slot on a shared class counter, so the order
+// of tied keys (and which destination gets which copies of a tie class split
+// across ranks) is unspecified; the receiver's sort orders them anyway, and
+// with width < word bits keys tied on the low bits may come out in a
+// different order from run to run.
 // ---------------------------------------------------------------------------
 template <typename K, int VB>
 struct ExchangeSmem {

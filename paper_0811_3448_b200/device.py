@@ -59,34 +59,66 @@ def stream_ptr(device=None) -> int:
 
 
 class _WorkspaceCache:
-    """Per-device grow-only workspace (a torch uint8 tensor from the caching allocator)."""
+    """Grow-only workspaces keyed by (device, stream), guarded by a lock.
+
+    A sort's workspace is live until its kernels finish, so two sorts in
+    flight on different streams (pool threads, like the reference's
+    ``sort_parallel`` workers, variants.py:195-206) must not share one: each
+    (device, stream) pair gets its own buffer, allocated on that stream so the
+    caching allocator orders its reuse with the stream's work.
+    """
 
     def __init__(self):
-        self._bufs = {}
+        import threading
 
-    def get(self, nbytes: int, device):
+        self._bufs = {}
+        self._lock = threading.Lock()
+
+    def get(self, nbytes: int, device, stream=None):
         t = torch()
         dev = t.device(device)
-        key = dev.index if dev.index is not None else t.cuda.current_device()
-        buf = self._bufs.get(key)
-        if buf is None or buf.numel() < nbytes:
-            buf = t.empty(max(int(nbytes), 256), dtype=t.uint8, device=dev)
-            self._bufs[key] = buf
-        return buf
+        idx = dev.index if dev.index is not None else t.cuda.current_device()
+        if stream is None:
+            stream = t.cuda.current_stream(idx)
+        key = (idx, stream.cuda_stream)
+        with self._lock:
+            buf = self._bufs.get(key)
+            if buf is None or buf.numel() < nbytes:
+                with t.cuda.device(idx), t.cuda.stream(stream):
+                    buf = t.empty(max(int(nbytes), 256), dtype=t.uint8, device=dev)
+                self._bufs[key] = buf
+            return buf
 
     def clear(self):
-        self._bufs.clear()
+        with self._lock:
+            self._bufs.clear()
+
+
+class SortOverflowError(RuntimeError):
+    """The device reported dropped work (bs_sort_status != 0): the output is not sorted."""
+
+
+def check_status(status) -> None:
+    """Raise if a device status word (CUDA int32[1] filled by bs_sort_status) is set (syncs)."""
+    v = int(status.item())
+    if v:
+        what = [n for b, n in ((1, "bucket list"), (2, "tile map"), (4, "task list")) if v & b]
+        raise SortOverflowError(f"device work-list overflow ({', '.join(what)}; status {v}): output is not sorted")
 
 
 workspaces = _WorkspaceCache()
 
 
 def sort_words_device(keys, vals=None, *, width: int, start_pos: int = 0, key_kind: int = 0,
-                      counters=None, depth: int = 1, workspace=None):
+                      counters=None, depth: int = 1, workspace=None, check: bool = True):
     """Sort a contiguous 1-D CUDA tensor of raw words in place (bs_sort).
 
     ``counters``: optional CUDA int64[4] tensor receiving the reference Metrics.
-    ``workspace``: optional CUDA uint8 tensor (defaults to the per-device cache).
+    ``workspace``: optional CUDA uint8 tensor (defaults to the (device, stream) cache).
+    ``check``: read the device overflow status back and raise
+    :class:`SortOverflowError` if work was dropped (one stream sync).  With
+    ``check=False`` the status tensor is returned for a deferred
+    :func:`check_status` (the timed bench loop).
     """
     t = require_cuda()
     if not keys.is_cuda or keys.dim() != 1 or not keys.is_contiguous():
@@ -114,7 +146,15 @@ def sort_words_device(keys, vals=None, *, width: int, start_pos: int = 0, key_ki
     with t.cuda.device(keys.device):
         rc = L.bs_sort(keys.data_ptr(), vptr, n, kb, vb, int(width), int(start_pos), int(key_kind),
                        workspace.data_ptr(), workspace.numel(), stream_ptr(keys.device), cptr, int(depth))
-    _lib.check(rc)
+        _lib.check(rc)
+        if n <= 1 or width - start_pos <= 0:
+            return None  # nothing launched
+        status = t.empty(1, dtype=t.int32, device=keys.device)
+        _lib.check(L.bs_sort_status(workspace.data_ptr(), status.data_ptr(), stream_ptr(keys.device)))
+    if check:
+        check_status(status)
+        return None
+    return status
 
 
 def metrics_device(sorted_keys, *, width: int, start_pos: int = 0, key_kind: int = 0, depth: int = 1,

@@ -157,7 +157,11 @@ class CudaOps:
             rc = L.bs_sort_from(bufs.local_keys, bufs.local_vals if vb else None, out_k.data_ptr(),
                                 out_v.data_ptr() if out_v is not None else None, count, kb, vb, self.width, 0,
                                 self.key_kind, ws.data_ptr(), ws.numel(), device.stream_ptr(dev))
-        _lib.check(rc)
+            _lib.check(rc)
+            if count > 1:
+                status = t.empty(1, dtype=t.int32, device=dev)
+                _lib.check(L.bs_sort_status(ws.data_ptr(), status.data_ptr(), device.stream_ptr(dev)))
+                device.check_status(status)
         return out_k, out_v
 
 
@@ -226,11 +230,13 @@ class PeerBuffers:
 
         L = _lib.lib()
         torch.cuda.synchronize(self.device)
-        _barrier(self.group, self.device)  # nobody still stores into or reads from these buffers
+        _host_barrier(self.group, self.device)  # nobody still stores into or reads from these buffers
         for p in self._peers:
-            L.bs_ipc_close(p)
-        _barrier(self.group, self.device)  # every peer mapping of our buffer is gone
-        L.bs_ipc_free(self._local)
+            _lib.check(L.bs_ipc_close(p))
+        # every peer has closed its mapping of our buffer (host-blocking: cudaFree
+        # of an exported region before the importers close it is undefined)
+        _host_barrier(self.group, self.device)
+        _lib.check(L.bs_ipc_free(self._local))
         self._local = None
         self._peers = []
         self.cap = 0
@@ -371,32 +377,79 @@ def _barrier(group, dev) -> None:
         dist.barrier(group=group)
 
 
+def _host_barrier(group, dev) -> None:
+    """Barrier that returns only when every rank has reached it AND its queued device work is done."""
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.synchronize(dev)
+    if _on_device(group):
+        dist.all_reduce(torch.zeros(1, device=dev), group=group)
+        torch.cuda.synchronize(dev)  # the NCCL all-reduce itself only orders the stream
+    else:
+        dist.barrier(group=group)
+
+
+MAX_RANKS = 8  # the split kernels classify into 2R-1 <= 15 classes (16-wide tile rows)
+
+
+def _single_node(group, R: int) -> bool:
+    """True when every rank of ``group`` runs on this host (CUDA IPC peer mappings need it)."""
+    import os
+    import socket
+
+    lws, ws = os.environ.get("LOCAL_WORLD_SIZE"), os.environ.get("WORLD_SIZE")
+    if lws is not None and ws is not None and int(ws) == R:
+        return int(lws) == int(ws)
+    import torch.distributed as dist
+
+    names = [None] * R
+    dist.all_gather_object(names, socket.gethostname(), group=group)
+    return len(set(names)) == 1
+
+
 def dist_sort(keys, values=None, *, width: int, key_kind: int = _lib.BS_KEY_UNSIGNED, ops=None, group=None,
-              samples_per_rank: int = 4096, exchange: str = "auto") -> DistResult:
+              samples_per_rank: int = 4096, exchange: str = "auto", marks: list | None = None) -> DistResult:
     """Globally sort the shards held by all ranks of ``group``.
 
     ``keys`` (and ``values``) are this rank's contiguous 1-D tensors (CUDA for
     the product path).  Returns this rank's slice of the global order; the
     concatenation over ranks 0..R-1 is the sorted whole.  ``exchange``:
     "peer" (fused partition + peer-memory stores, the product path for CUDA
-    tensors), "collective" (partition + all-to-all-v), or "auto".
+    tensors on one node), "collective" (partition + all-to-all-v), or "auto"
+    ("peer" for CUDA tensors when every rank is on this node, else
+    "collective").  ``marks`` (instrumentation): a list that receives
+    ``(phase, cuda.Event)`` pairs recorded on the current stream at the phase
+    boundaries of the peer path (bench.py's per-phase roofline).
+
+    Scope: one NVLink/NVSwitch node of at most ``MAX_RANKS`` (8) GPUs -- the
+    B200 HGX node the fused exchange is built for.  Larger groups raise
+    ``ValueError`` up front; "peer" across nodes raises ``ValueError`` (CUDA
+    IPC mappings do not cross hosts).
     """
     import torch
     import torch.distributed as dist
 
     ops = ops or CudaOps(width, key_kind)
-    if exchange == "auto":
-        exchange = "peer" if isinstance(ops, CudaOps) and getattr(keys, "is_cuda", False) else "collective"
-    if exchange not in ("peer", "collective"):
+    if exchange not in ("auto", "peer", "collective"):
         raise ValueError(f"unknown exchange {exchange!r}")
     R = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if R > MAX_RANKS:
+        raise ValueError(f"dist_sort supports at most {MAX_RANKS} ranks (one NVSwitch node), got {R}")
+    if exchange != "collective" and R > 1:
+        cuda_path = isinstance(ops, CudaOps) and getattr(keys, "is_cuda", False)
+        one_node = cuda_path and _single_node(group, R)
+        if exchange == "auto":
+            exchange = "peer" if one_node else "collective"
+        elif not one_node:
+            raise ValueError("exchange='peer' needs CUDA tensors and every rank on one node (CUDA IPC)")
     if R == 1:
         k, v = ops.sort(keys, values)
         return DistResult(k, v, [keys.numel()], [keys.numel()])
     dev = keys.device
     if exchange == "peer":
-        return _dist_sort_peer(keys, values, ops, group, R, rank, samples_per_rank)
+        return _dist_sort_peer(keys, values, ops, group, R, rank, samples_per_rank, marks)
     # 1. splitters from gathered samples
     smp = ops.sample(keys, samples_per_rank if keys.numel() else 0)
     cnt = torch.tensor([smp.numel()], dtype=torch.int64, device=dev)
@@ -447,11 +500,18 @@ def _all_gather_dev(t, group):
     return torch.stack(parts)
 
 
-def _dist_sort_peer(keys, values, ops, group, R: int, rank: int, S: int) -> DistResult:
+def _dist_sort_peer(keys, values, ops, group, R: int, rank: int, S: int, marks=None) -> DistResult:
     """dist_sort with the fused partition + peer-store exchange (one host sync per call)."""
     import torch
 
+    def mark(name):
+        if marks is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            marks.append((name, ev))
+
     dev = keys.device
+    mark("start")
     # 1. splitters on the device: S normalised samples per rank (an empty shard
     # contributes the maximum word), all-gathered, sorted, quantiles i*S
     if keys.numel():
@@ -460,19 +520,26 @@ def _dist_sort_peer(keys, values, ops, group, R: int, rank: int, S: int) -> Dist
         smp = torch.full((S,), -1, dtype=keys.dtype, device=dev)
     ssorted = ops.sort_samples(_all_gather_dev(smp, group).reshape(-1))
     splitters = ssorted[torch.arange(1, R, device=dev) * S].contiguous()  # == choose_splitters
+    mark("splitters")
     # 2+3. class counts of every shard; the one host read also orders this
     # rank's previous local sort (which reads its receive buffer) before the
     # all-gather completes anywhere, so no peer overwrites a buffer in use
-    cc = _all_gather_dev(ops.split_count(keys, splitters, R), group).cpu().numpy().astype(np.int64)
+    counts = ops.split_count(keys, splitters, R)
+    mark("class_count")
+    cc = _all_gather_dev(counts, group).cpu().numpy().astype(np.int64)
     B, delta, rcounts = exchange_plan(cc, R, rank)
     kb = keys.element_size()
     vb = values.element_size() if values is not None else 0
     bufs = _peer_buffers(group, dev).ensure(int(rcounts.max()), kb, vb)
     # 4. fused partition + peer stores, then every rank's stores land
+    mark("plan")
     ops.exchange(keys, values, splitters, R, delta, B, bufs)
+    mark("exchange")
     _barrier(group, dev)
+    mark("barrier")
     # 5. local sort out of the receive buffer
     out_k, out_v = ops.sort_from(bufs, int(rcounts[rank]), keys.dtype, values.dtype if values is not None else None)
+    mark("local_sort")
     scounts = send_counts(cc, B, rank)
     return DistResult(out_k, out_v, scounts, [send_counts(cc, B, src)[rank] for src in range(R)])
 

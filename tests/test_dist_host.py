@@ -217,3 +217,39 @@ def test_device_splitter_indices_match_choose_splitters(R, S):
     device; that is choose_splitters() on the R*S gathered samples."""
     s = np.arange(R * S, dtype=np.uint64) * np.uint64(3)
     assert np.array_equal(choose_splitters(s, R), s[np.arange(1, R) * S])
+
+
+def test_dist_sort_rejects_more_than_eight_ranks(monkeypatch):
+    import torch
+    import torch.distributed as tdist
+
+    from paper_0811_3448_b200 import dist as bd
+
+    monkeypatch.setattr(tdist, "is_initialized", lambda: True)
+    monkeypatch.setattr(tdist, "get_world_size", lambda group=None: 9)
+    monkeypatch.setattr(tdist, "get_rank", lambda group=None: 0)
+    with pytest.raises(ValueError, match="at most 8 ranks"):
+        bd.dist_sort(torch.zeros(4, dtype=torch.int32), width=32)
+
+
+def test_single_node_detection(monkeypatch):
+    from paper_0811_3448_b200 import dist as bd
+
+    monkeypatch.setenv("WORLD_SIZE", "4")
+    monkeypatch.setenv("LOCAL_WORLD_SIZE", "4")
+    assert bd._single_node(None, 4)
+    monkeypatch.setenv("LOCAL_WORLD_SIZE", "2")
+    assert not bd._single_node(None, 4)
+
+
+def test_peer_exchange_refused_for_cpu_tensors(monkeypatch):
+    import torch
+    import torch.distributed as tdist
+
+    from paper_0811_3448_b200 import dist as bd
+
+    monkeypatch.setattr(tdist, "is_initialized", lambda: True)
+    monkeypatch.setattr(tdist, "get_world_size", lambda group=None: 2)
+    monkeypatch.setattr(tdist, "get_rank", lambda group=None: 0)
+    with pytest.raises(ValueError, match="peer"):
+        bd.dist_sort(torch.zeros(4, dtype=torch.int32), width=32, exchange="peer")

@@ -194,9 +194,113 @@ def test_bench_two_ranks_share_one_gpu():
     env = dict(os.environ, BS_BENCH_SHARE_GPU="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
-           "--steps", "2", "--warmup", "3", "--keys-per-rank", str(1 << 22)]
-    p = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=500)
-    assert p.returncode == 0, p.stderr[-2000:]
-    line = [ln for ln in p.stdout.splitlines() if ln.startswith("{")][-1]
-    r = json.loads(line)
-    assert r["n_gpus"] == 2 and r["config"]["global_batch"] == 2 << 22 and r["value"] > 0
+           "--steps", "2", "--warmup", "3"]
+    for extra, total, scaling in ((["--config", "cfg2", "--keys-per-rank", str(1 << 22)], 2 << 22, "weak"),
+                                  (["--total", str(3 << 22)], 3 << 22, "strong")):
+        p = subprocess.run(cmd + extra, cwd=root, env=env, capture_output=True, text=True, timeout=500)
+        assert p.returncode == 0, p.stderr[-2000:]
+        line = [ln for ln in p.stdout.splitlines() if ln.startswith("{")][-1]
+        r = json.loads(line)
+        assert r["n_gpus"] == 2 and r["config"]["global_batch"] == total and r["value"] > 0
+        assert r["scaling"] == scaling and r["sort_roofline"]["t_roof_ms"] > 0 and r["e2e"]["value"] > 0
+
+
+# --------------------------------------------------------------------------
+# cfg5 at full size (BASELINE configs[4]): 2^30 uint32 keys from MT19937(4)
+# in contiguous N/R slices, plus the already-sorted and reverse-sorted
+# adversarial inputs, through the real per-rank device steps of the fused
+# exchange with R = 2/4/8 emulated ranks on one B200.  The concatenated
+# per-rank outputs must hash to the reference's own output (golden.json,
+# reference variants.sort_parallel at 2^30, variants.py:162-229).
+# --------------------------------------------------------------------------
+
+_CFG5 = {}
+
+
+def _cfg5_input(kind):
+    from paper_0811_3448_b200 import cases
+
+    if "uniform" not in _CFG5:
+        _CFG5["uniform"] = cases.config5("uniform")
+    x = _CFG5["uniform"]
+    if kind == "uniform":
+        return x
+    if "sorted" not in _CFG5:
+        _CFG5["sorted"] = np.sort(x)
+    s = _CFG5["sorted"]
+    return s if kind == "sorted" else s[::-1]
+
+
+def _emulated_hash(x, R):
+    """Run the emulated R-rank fused exchange over contiguous slices of x; stream-hash the output."""
+    import hashlib
+
+    import torch
+
+    n = x.size
+    offs = [(r * n) // R for r in range(R + 1)]
+    ops = CudaOps(32)
+    keys = [torch.from_numpy(np.ascontiguousarray(x[offs[r]:offs[r + 1]]).view(np.int32)).cuda() for r in range(R)]
+    smp = torch.cat([ops.sample(k, 4096) for k in keys])
+    ss = ops.sort_samples(smp)
+    spl = ss[torch.arange(1, R, device="cuda") * 4096].contiguous()  # == choose_splitters
+    per_src = [CudaOps(32) for _ in range(R)]
+    cc = np.array([per_src[r].split_count(keys[r], spl, R).cpu().numpy() for r in range(R)], dtype=np.int64)
+    _, _, rcounts = exchange_plan(cc, R, 0)
+    recv = [torch.empty(max(1, int(c)), dtype=torch.int32, device="cuda") for c in rcounts]
+    bufs = types.SimpleNamespace(
+        key_table=torch.tensor([t.data_ptr() for t in recv], dtype=torch.int64, device="cuda"), val_table=None)
+    for r in range(R):
+        B, delta, _ = exchange_plan(cc, R, r)
+        per_src[r].exchange(keys[r], None, spl, R, delta, B, bufs)
+    del keys
+    h = hashlib.sha256()
+    sizes = []
+    for d in range(R):
+        b = types.SimpleNamespace(device=recv[d].device, local_keys=recv[d].data_ptr(), local_vals=None)
+        k, _ = ops.sort_from(b, int(rcounts[d]), torch.int32, None)
+        h.update(k.cpu().numpy().view(np.uint32).tobytes())
+        sizes.append(k.numel())
+        del k
+    return h.hexdigest(), sizes
+
+
+@pytest.mark.slow
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("R", [2, 4, 8])
+@pytest.mark.parametrize("kind", ["uniform", "sorted", "reverse"])
+def test_cfg5_full_size_emulated_ranks(golden, R, kind):
+    g = golden.get("big", {})
+    if "cfg5" not in g:
+        pytest.skip("golden.json was generated without --big")
+    x = _cfg5_input(kind)
+    want_in = {"uniform": g["cfg5"], "sorted": g["cfg5_sorted"], "reverse": g["cfg5_reverse"]}[kind]["input_sha"]
+    if R == 2:  # pin the generated input once per kind
+        import hashlib
+
+        assert hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest() == want_in
+    digest, sizes = _emulated_hash(x, R)
+    assert digest == g["cfg5"]["output_sha"]
+    assert sum(sizes) == x.size
+    # destination loads stay balanced on every input order (same multiset)
+    assert max(sizes) - min(sizes) <= 0.02 * x.size / R, sizes
+
+
+@pytest.mark.parametrize("R", [2, 4, 8])
+def test_sampler_misled_by_a_hidden_outlier(R):
+    """A single key with the top bits set at an index no strided sample sees,
+    and a shard whose samples are all equal: the splitters are wrong for the
+    data, but every key must still land in the right global position."""
+    rng = np.random.default_rng(77 + R)
+    shards = []
+    for r in range(R):
+        n = (1 << 18) + 7 * r
+        k = np.full(n, 0x00010000, dtype=np.uint32) + rng.integers(0, 3, n).astype(np.uint32)
+        k[1] = 0xFFFFFFFF  # strided samples sit at (2i+1)n/2S: index 1 is never sampled for these n
+        if r == R - 1:
+            k[:] = 0x00010001
+            k[2] = 0xFFFFFFF0
+        shards.append(k)
+    outs, _ = _emulated(shards, None, R)
+    got = np.concatenate([o[0] for o in outs])
+    assert np.array_equal(got, np.sort(np.concatenate(shards)))

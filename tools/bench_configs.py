@@ -63,9 +63,11 @@ def run(name: str, reps: int, with_phases: bool = True, warmup: int = 3):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        device.sort_words_device(kdev, vdev, width=kb * 8, workspace=ws)
+        st = device.sort_words_device(kdev, vdev, width=kb * 8, workspace=ws, check=False)
         e1.record()
         torch.cuda.synchronize()
+        if st is not None:
+            device.check_status(st)
         if r >= warmup:
             times.append(e0.elapsed_time(e1))
     phases = {}
