@@ -238,6 +238,47 @@ int bs_sample_keys(const void *keys, uint64_t n, int key_bytes, int width,
                    int key_kind, uint64_t count, void *out_samples,
                    void *stream);
 
+/* -------------------------------------------------------------------------
+ * Exact reference-order engine.  Replays the reference recursion bit level
+ * by bit level with the exact two-cursor permutation of every partition
+ * (kernels.py:56-77), so the output -- including the
+ * order of keys equal in the examined bits, and values carried alongside --
+ * and the counters are the reference's own for every drive form:
+ *
+ *   mode 0  kernels.sort_words(arr, lo, up, start_pos, width, passthrough_loop,
+ *           check_after, streak, checked, counters, depth)   (kernels.py:88-126)
+ *           -- core.sort / variants.sort_optimized / binar_sort_range
+ *   mode 1  kernels.sort_words_iterative(arr, lo, up, width, counters)
+ *           (kernels.py:129-172; max_depth = stack high-water mark)
+ *   mode 2  core._sort_levels (core.py:146-180): a sortedness scan before every
+ *           partition, one call per partition; `on_level` is called after each
+ *           level's kernels are enqueued (sort_with_observer)
+ *   mode 3  variants.sort_parallel (variants.py:162-229): `par_levels` levels
+ *           of _prepartition, then sort_words per bucket from pos=par_levels
+ *
+ * The sort key is (enc(x) << pos) & (1 << (width-1)) with enc the key_kind
+ * transform of the raw word; sortedness scans compare whole encoded words,
+ * like range_sorted_words (kernels.py:80-85).  counters (device int64[4], may
+ * be NULL) is overwritten.  n < 2^32 - 1.  Slower than bs_sort (width passes
+ * of ~40 bytes per element instead of ~4 digit passes): bs_sort is the
+ * product path wherever the tie order cannot be observed.
+ * ------------------------------------------------------------------------- */
+typedef void (*bs_level_fn)(void *ctx, int pos);
+size_t bs_exact_workspace_bytes(uint64_t n, int key_bytes, int val_bytes);
+int bs_exact_sort(void *keys, void *vals, uint64_t n, int key_bytes, int val_bytes,
+                  int width, int start_pos, int key_kind, int mode,
+                  int passthrough_loop, int check_after, int streak, int checked,
+                  int par_levels, int64_t depth, void *ws, size_t ws_bytes,
+                  void *stream, int64_t *counters, bs_level_fn on_level, void *ctx);
+/*
+ * Start positions (ascending, relative to keys) of the engine's current
+ * segments -- the reference observer's (lower, upper) list (core.py:175-180)
+ * -- written to starts (device uint32[n]); their number to *count (device).
+ * Call from on_level (same ws, n, key_bytes, val_bytes, stream).
+ */
+int bs_exact_boundaries(const void *ws, uint64_t n, int key_bytes, int val_bytes,
+                        uint32_t *starts, uint32_t *count, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

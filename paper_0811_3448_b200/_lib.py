@@ -17,10 +17,13 @@ _ROOT = os.path.dirname(_HERE)
 SO_PATH = os.path.join(_HERE, "libbinarsort_b200.so")
 _CSRC = os.path.join(_HERE, "csrc")
 _SOURCES = ["binarsort_b200.cu"]
-_DEPS = ["binarsort_b200.cu", "common.cuh", "sort_impl.cuh", "dense_impl.cuh", "metrics_impl.cuh", "misc_impl.cuh"]
+_DEPS = ["binarsort_b200.cu", "common.cuh", "sort_impl.cuh", "dense_impl.cuh", "metrics_impl.cuh", "misc_impl.cuh",
+         "exact_impl.cuh"]
 
 BS_OK, BS_ERR_VALUE, BS_ERR_ASSERT, BS_ERR_CUDA, BS_ERR_WORKSPACE, BS_ERR_INTERNAL = range(6)
 BS_KEY_UNSIGNED, BS_KEY_SIGNED, BS_KEY_FLOAT = 0, 1, 2
+EX_REC, EX_ITER, EX_LEVELS, EX_PAR = 0, 1, 2, 3  # bs_exact_sort modes
+LEVEL_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int)  # bs_level_fn
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
@@ -35,7 +38,8 @@ EXPORTS = (
     "bs_split_by_splitters", "bs_sample_keys", "bs_sort_profiled", "bs_sort_launches",
     "bs_sort_from_workspace_bytes", "bs_sort_from", "bs_split_count", "bs_split_exchange",
     "bs_ipc_handle_bytes", "bs_ipc_alloc", "bs_ipc_open", "bs_ipc_close", "bs_ipc_free",
-    "bs_sort_status", "bs_debug_capacity",
+    "bs_sort_status", "bs_debug_capacity", "bs_exact_workspace_bytes", "bs_exact_sort",
+    "bs_exact_boundaries",
 )
 
 
@@ -129,6 +133,13 @@ def lib() -> ctypes.CDLL:
         L.bs_sort_status.restype = i32
         L.bs_debug_capacity.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32]
         L.bs_debug_capacity.restype = None
+        L.bs_exact_workspace_bytes.argtypes = [u64, i32, i32]
+        L.bs_exact_workspace_bytes.restype = sz
+        L.bs_exact_sort.argtypes = [vp, vp, u64, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, i64,
+                                    vp, sz, vp, vp, LEVEL_FN, vp]
+        L.bs_exact_sort.restype = i32
+        L.bs_exact_boundaries.argtypes = [vp, u64, i32, i32, vp, vp, vp]
+        L.bs_exact_boundaries.restype = i32
         _lib = L
         return L
 

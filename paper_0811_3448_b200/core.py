@@ -253,14 +253,21 @@ class _Encoder:
 
 
 def binar_sort_range(seq, rng: SortRange, codec, metrics: Metrics, observer=None) -> None:
-    """Sort ``seq[rng.lower..rng.upper]`` in place from bit ``rng.pos`` (core.py:183-198)."""
+    """Sort ``seq[rng.lower..rng.upper]`` in place from bit ``rng.pos`` (core.py:183-198).
+
+    With an ``observer`` the level-synchronous engine runs and reports the
+    sub-array boundaries after every bit level (core.py:146-180), exactly as
+    the reference's does (same partitions, same sortedness stops, same
+    counters).
+    """
     assert rng.is_empty() or (rng.lower >= 0 and rng.upper < len(seq)), "range exceeds sequence bounds"
     if rng.is_empty():
         return
     width = codec.width_for(seq)
     assert rng.pos <= width, "bit position past codec width"
     if observer is not None:
-        raise NotImplementedError("per-level observer tracing is outside the B200 hot path (SURVEY §8f)")
+        _sort_levels_device(seq, codec, width, rng.lower, rng.upper, rng.pos, metrics, observer)
+        return
     n = rng.upper - rng.lower + 1
     if n < 2 or rng.pos == width:
         # the reference's base case still counts one call at depth 1 (kernels.py:100-105)
@@ -270,27 +277,74 @@ def binar_sort_range(seq, rng: SortRange, codec, metrics: Metrics, observer=None
     _sort_device(seq, codec, None, width, rng.pos, 1, metrics, rng.lower, rng.upper)
 
 
+def _word_bits(w) -> int:
+    return w.keys.element_size() * 8
+
+
+def _tie_order_observable(w, width: int, start_pos: int) -> bool:
+    """Could two words equal in the examined key bits differ elsewhere?
+
+    Only then does the order among equal keys show in a keys-only result; the
+    fast sort (unique nondecreasing output) is bit-exact otherwise.
+    """
+    return start_pos > 0 or width < _word_bits(w)
+
+
 def _sort_device(seq, codec, values, width, start_pos, depth, metrics, lower=0, upper=None,
-                 with_metrics=True):
+                 with_metrics=True, exact=None, mode=None, **exact_kw):
     if codec.gpu_spec(seq) is None:  # generic-engine element types: out of scope
         raise TypeError(f"{type(codec).__name__} on {type(seq).__name__} has no word view "
                         "(the B200 backend sorts 1-D integer/float arrays, tensors and lists)")
     t = device.require_cuda()
     w = DeviceWords(seq, codec, values, lower=lower, upper=upper)
     counters = t.zeros(4, dtype=t.int64, device=w.keys.device) if with_metrics else None
-    device.sort_words_device(w.keys, w.vals, width=width, start_pos=start_pos, key_kind=w.key_kind,
-                             counters=counters, depth=depth)
+    if exact is None:
+        exact = mode is not None or (values is None and _tie_order_observable(w, width, start_pos))
+    if exact:
+        device.exact_sort_device(w.keys, w.vals, width=width, start_pos=start_pos, key_kind=w.key_kind,
+                                 mode=_lib.EX_REC if mode is None else mode, depth=depth, counters=counters,
+                                 **exact_kw)
+    else:
+        device.sort_words_device(w.keys, w.vals, width=width, start_pos=start_pos, key_kind=w.key_kind,
+                                 counters=counters, depth=depth)
     w.commit()
     if with_metrics and metrics is not None:
         metrics._add_counters(counters.cpu().numpy())
 
 
-def sort(seq, codec, values=None, *, with_metrics: bool = True) -> Metrics:
+def _sort_levels_device(seq, codec, width, lower, upper, start_pos, metrics, observer):
+    """core._sort_levels (core.py:146-180) on the device: the observer sees (pos, [(lo, up), ...])."""
+    n = upper - lower + 1
+
+    def on_level(pos, starts):
+        ends = np.empty(len(starts), dtype=np.int64)
+        ends[:-1] = starts[1:].astype(np.int64) - 1
+        if len(starts):
+            ends[-1] = n - 1
+        observer(pos, [(lower + int(a), lower + int(b)) for a, b in zip(starts, ends)])
+
+    if start_pos >= width:
+        return
+    if n < 2:  # segments = [(lower, upper, False)]: no work, the observer still sees every level
+        for pos in range(start_pos, width):
+            observer(pos, [(lower, upper)])
+        return
+    _sort_device(seq, codec, None, width, start_pos, 1, metrics, lower, upper, mode=_lib.EX_LEVELS,
+                 on_level=on_level)
+
+
+def sort(seq, codec, values=None, *, with_metrics: bool = True, exact: bool | None = None) -> Metrics:
     """Sort ``seq`` in place into nondecreasing codec order; return Metrics (core.py:201-222).
 
     ``values`` (extension): a same-length sequence permuted alongside the
-    keys.  The device sort is stable, so equal keys keep their input order
-    and every value stays with its key.
+    keys.  By default the device sort is stable, so equal keys keep their
+    input order and every value stays with its key.
+
+    ``exact``: ``None`` (default) picks the fast digit sort whenever the
+    order of equal keys cannot be observed (keys only, full-width words) and
+    the exact reference-order engine otherwise (``UnsignedCodec(w)`` on wider
+    words, lists); ``True`` always replays the reference's own (unstable)
+    permutations -- also for ``values``; ``False`` always takes the fast sort.
     """
     metrics = Metrics()
     n = len(seq)
@@ -299,10 +353,22 @@ def sort(seq, codec, values=None, *, with_metrics: bool = True) -> Metrics:
     width = codec.width_for(seq)
     if width == 0:
         return metrics
-    _sort_device(seq, codec, values, width, 0, 1, metrics, with_metrics=with_metrics)
+    _sort_device(seq, codec, values, width, 0, 1, metrics, with_metrics=with_metrics, exact=exact)
     return metrics
 
 
-def sort_with_observer(seq, codec, observer) -> Metrics:  # pragma: no cover - out of scope
-    """Per-bit-level trace (core.py:225-239): outside the B200 hot path."""
-    raise NotImplementedError("sort_with_observer is outside the B200 hot path (SURVEY §8f rank 4)")
+def sort_with_observer(seq, codec, observer) -> Metrics:
+    """Sort ``seq`` while reporting sub-array boundaries per bit level (core.py:225-239).
+
+    The observer is called once per bit position with ``(pos, boundaries)``.
+    Inputs of fewer than two elements sort trivially with no callbacks.
+    """
+    metrics = Metrics()
+    n = len(seq)
+    if n <= 1:
+        return metrics
+    width = codec.width_for(seq)
+    if width == 0:
+        return metrics
+    _sort_levels_device(seq, codec, width, 0, n - 1, 0, metrics, observer)
+    return metrics

@@ -14,6 +14,7 @@
 #include "misc_impl.cuh"
 #include "sort_impl.cuh"
 #include "dense_impl.cuh"
+#include "exact_impl.cuh"
 
 namespace bs {
 
@@ -783,3 +784,190 @@ int bs_sample_keys(const void *keys, uint64_t n, int key_bytes, int width, int k
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Exact reference-order engine (exact_impl.cuh): host driver.
+// ---------------------------------------------------------------------------
+namespace bs {
+
+struct ExLayout {
+  size_t copy, vcopy, seg, tab0, tab1, lone, zpos, bcnt, ctr, total;
+  uint64_t nblk;
+};
+
+static ExLayout ex_layout(uint64_t n, int kb, int vb) {
+  ExLayout l{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += align_up(bytes);
+    return o;
+  };
+  l.nblk = (n + ex::EX_CHUNK - 1) / ex::EX_CHUNK;
+  l.ctr = take(4 * sizeof(unsigned long long));
+  l.bcnt = take(sizeof(uint32_t) * (l.nblk + 1));
+  l.seg = take(sizeof(uint32_t) * n);
+  l.tab0 = take(sizeof(ex::SegT) * n);
+  l.tab1 = take(sizeof(ex::SegT) * n);
+  l.lone = take(sizeof(uint32_t) * (n + 1));
+  l.zpos = take(sizeof(uint32_t) * (n + 1));
+  l.copy = take(size_t(kb) * n);
+  l.vcopy = take(size_t(vb) * n);
+  l.total = off;
+  return l;
+}
+
+template <typename K, int VB>
+static int run_exact(void *keys, void *vals, uint64_t n, int width, int pos0, int key_kind, int mode, int loop,
+                     int check_after, int streak0, int checked0, int par_levels, int64_t depth0, void *wsp,
+                     size_t ws_bytes, cudaStream_t st, int64_t *counters, bs_level_fn on_level, void *ctx) {
+  const ExLayout l = ex_layout(n, int(sizeof(K)), VB);
+  if (ws_bytes < l.total)
+    return fail(BS_ERR_WORKSPACE, "workspace too small: need " + std::to_string(l.total) + " bytes, got " +
+                                      std::to_string(ws_bytes));
+  char *b = static_cast<char *>(wsp);
+  ex::Ex e{};
+  e.keys[0] = keys;
+  e.keys[1] = b + l.copy;
+  e.vals[0] = vals;
+  e.vals[1] = VB ? b + l.vcopy : nullptr;
+  e.seg = reinterpret_cast<uint32_t *>(b + l.seg);
+  e.tab[0] = reinterpret_cast<ex::SegT *>(b + l.tab0);
+  e.tab[1] = reinterpret_cast<ex::SegT *>(b + l.tab1);
+  e.lone = reinterpret_cast<uint32_t *>(b + l.lone);
+  e.zpos = reinterpret_cast<uint32_t *>(b + l.zpos);
+  e.bcnt = reinterpret_cast<uint32_t *>(b + l.bcnt);
+  e.ctr = counters ? reinterpret_cast<unsigned long long *>(counters)
+                   : reinterpret_cast<unsigned long long *>(b + l.ctr);
+  e.n = n;
+  e.width = width;
+  e.kind = key_kind;
+  e.mode = mode;
+  e.loop = loop;
+  e.check_after = check_after;
+  e.par_levels = par_levels;
+  e.depth0 = mode == ex::M_PAR ? 0 : depth0;
+  const int nlev = width - pos0;
+  // root record and counters before the first level (see exact_impl.cuh)
+  int64_t c0[4] = {0, 0, 0, 0};
+  uint32_t rbits = 0;
+  if (mode == ex::M_REC) {  // the root call (kernels.py:100-102)
+    c0[2] = 1;
+    c0[3] = depth0;
+    rbits = (n >= 2 && nlev > 0) ? ex::F_ACTIVE : 0u;
+    if (checked0) rbits |= ex::F_CHECKED;
+  } else if (mode == ex::M_ITER) {  // the stack holds the root (kernels.py:138-142)
+    c0[3] = 1;
+    rbits = (n >= 1 && nlev > 0) ? ex::F_ACTIVE : 0u;
+  } else if (mode == ex::M_LEVELS) {  // core.py:157: segments = [(lower, upper, upper > lower)]
+    rbits = n >= 2 ? (ex::F_ACTIVE | ex::F_CHECK) : 0u;
+  } else {  // sort_parallel: prepartition levels (variants.py:181-193), then bucket calls
+    if (n >= 2) {
+      c0[3] = par_levels;
+      if (par_levels == 0) {  // one bucket: sort_words(words, 0, n-1, 0, width, ..., 1)
+        c0[2] = 1;
+        c0[3] = 1;
+      }
+    }
+    rbits = (n >= 2 && nlev > 0) ? ex::F_ACTIVE : 0u;
+  }
+  const uint32_t rdep = (mode == ex::M_PAR && par_levels == 0) ? 1u : 0u;
+  const ex::SegT root{uint32_t(n), ex::pack(rbits, uint32_t(streak0), rdep, 0), 0, 0};
+  BS_CUDA(cudaMemcpyAsync(e.ctr, c0, sizeof(c0), cudaMemcpyHostToDevice, st));
+  if (n == 0) return BS_OK;
+  const unsigned g1 = unsigned(min64((n + 255) / 256, uint64_t(1) << 30));
+  const unsigned gchunk = unsigned(l.nblk);
+  ex::ex_init_kernel<<<unsigned(min64((n + 255) / 256, uint64_t(num_sms()) * 16)), 256, 0, st>>>(e, root);
+  const bool checks = (mode == ex::M_REC && check_after > 0) || mode == ex::M_LEVELS;
+  for (int L = 0; L < nlev; ++L) {
+    const int pos = pos0 + L, par = L & 1, cur = L & 1;
+    if (checks) ex::ex_check_kernel<K><<<g1, 256, 0, st>>>(e, par, cur);
+    ex::ex_count_kernel<K><<<gchunk, ex::EX_BLOCK, 0, st>>>(e, pos, par, cur);
+    scan_blocks_kernel<<<1, 1024, 0, st>>>(e.bcnt, uint32_t(l.nblk), nullptr);
+    ex::ex_bounds_kernel<K><<<gchunk, ex::EX_BLOCK, 0, st>>>(e, pos, par, cur);
+    ex::ex_plan_kernel<<<g1, 256, 0, st>>>(e, L, pos, cur);
+    ex::ex_index_kernel<K><<<gchunk, ex::EX_BLOCK, 0, st>>>(e, pos, par, cur);
+    ex::ex_gather_kernel<K, VB><<<gchunk, ex::EX_BLOCK, 0, st>>>(e, pos, par, cur);
+    BS_CUDA(cudaGetLastError());
+    if (on_level) on_level(ctx, pos);
+  }
+  const int fcur = nlev & 1;
+  if (mode == ex::M_REC && check_after > 0) {  // scans flagged by the last level
+    ex::ex_check_kernel<K><<<g1, 256, 0, st>>>(e, fcur, fcur);
+    ex::ex_resolve_kernel<<<g1, 256, 0, st>>>(e, fcur);
+  }
+  ex::ex_finalize_kernel<K, VB><<<unsigned(min64((n + 255) / 256, uint64_t(num_sms()) * 16)), 256, 0, st>>>(
+      e, fcur, uint32_t(nlev & 1));
+  BS_CUDA(cudaGetLastError());
+  return BS_OK;
+}
+
+}  // namespace bs
+
+extern "C" {
+
+size_t bs_exact_workspace_bytes(uint64_t n, int key_bytes, int val_bytes) {
+  if ((key_bytes != 4 && key_bytes != 8) || (val_bytes != 0 && val_bytes != 4 && val_bytes != 8)) return 0;
+  return ex_layout(n, key_bytes, val_bytes).total;
+}
+
+int bs_exact_sort(void *keys, void *vals, uint64_t n, int key_bytes, int val_bytes, int width, int start_pos,
+                  int key_kind, int mode, int passthrough_loop, int check_after, int streak, int checked,
+                  int par_levels, int64_t depth, void *ws, size_t ws_bytes, void *stream, int64_t *counters,
+                  bs_level_fn on_level, void *ctx) {
+  if (key_bytes != 4 && key_bytes != 8) return fail(BS_ERR_VALUE, "key_bytes must be 4 or 8");
+  if (val_bytes != 0 && val_bytes != 4 && val_bytes != 8) return fail(BS_ERR_VALUE, "val_bytes must be 0, 4 or 8");
+  if (width < 1 || width > key_bytes * 8) return fail(BS_ERR_VALUE, "unsupported word width " + std::to_string(width));
+  if (start_pos < 0 || start_pos > width) return fail(BS_ERR_ASSERT, "bit position past codec width");
+  if (key_kind < 0 || key_kind > 2) return fail(BS_ERR_VALUE, "unknown key_kind");
+  if (key_kind == BS_KEY_SIGNED && width < 2) return fail(BS_ERR_VALUE, "unsupported word width " + std::to_string(width));
+  if (key_kind == BS_KEY_FLOAT && width != 64) return fail(BS_ERR_VALUE, "float keys are 64-bit words of width 64");
+  if (mode < 0 || mode > 3) return fail(BS_ERR_VALUE, "unknown exact mode");
+  if (check_after < 0) return fail(BS_ERR_VALUE, "sortedness_check_after must be >= 0");
+  if (par_levels < 0 || par_levels > width || (mode == 3 && start_pos != 0))
+    return fail(BS_ERR_VALUE, "bad prepartition levels");
+  if (n >= (uint64_t(1) << 32) - 1) return fail(BS_ERR_VALUE, "n too large for the exact engine");
+  if (n > 0 && keys == nullptr) return fail(BS_ERR_VALUE, "NULL key buffer");
+  if (val_bytes != 0 && n > 0 && vals == nullptr) return fail(BS_ERR_VALUE, "val_bytes > 0 but vals is NULL");
+  if (depth < 0 || depth > 120) return fail(BS_ERR_VALUE, "depth out of range");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (val_bytes == 0) vals = nullptr;
+  streak = streak < 0 ? 0 : (streak > 255 ? 255 : streak);
+#define BS_EX(K)                                                                                                    \
+  do {                                                                                                              \
+    if (val_bytes == 0)                                                                                             \
+      return run_exact<K, 0>(keys, vals, n, width, start_pos, key_kind, mode, passthrough_loop, check_after, streak, \
+                             checked, par_levels, depth, ws, ws_bytes, st, counters, on_level, ctx);                \
+    if (val_bytes == 4)                                                                                             \
+      return run_exact<K, 4>(keys, vals, n, width, start_pos, key_kind, mode, passthrough_loop, check_after, streak, \
+                             checked, par_levels, depth, ws, ws_bytes, st, counters, on_level, ctx);                \
+    return run_exact<K, 8>(keys, vals, n, width, start_pos, key_kind, mode, passthrough_loop, check_after, streak,   \
+                           checked, par_levels, depth, ws, ws_bytes, st, counters, on_level, ctx);                  \
+  } while (0)
+  if (key_bytes == 4) BS_EX(uint32_t);
+  BS_EX(uint64_t);
+#undef BS_EX
+}
+
+int bs_exact_boundaries(const void *ws, uint64_t n, int key_bytes, int val_bytes, uint32_t *starts, uint32_t *count,
+                        void *stream) {
+  if (!ws || !starts || !count) return fail(BS_ERR_VALUE, "ws, starts and count must be non-NULL");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (n == 0) {
+    BS_CUDA(cudaMemsetAsync(count, 0, sizeof(uint32_t), st));
+    return BS_OK;
+  }
+  const ExLayout l = ex_layout(n, key_bytes, val_bytes);
+  const char *b = static_cast<const char *>(ws);
+  const uint32_t *seg = reinterpret_cast<const uint32_t *>(b + l.seg);
+  // the chunk counts reuse the engine's bcnt array (the level's kernels are done with it)
+  uint32_t *bcnt = reinterpret_cast<uint32_t *>(const_cast<char *>(b) + l.bcnt);
+  ex::ex_starts_count_kernel<<<unsigned(l.nblk), ex::EX_BLOCK, 0, st>>>(seg, n, bcnt);
+  scan_blocks_kernel<<<1, 1024, 0, st>>>(bcnt, uint32_t(l.nblk), count);
+  ex::ex_starts_write_kernel<<<unsigned(l.nblk), ex::EX_BLOCK, 0, st>>>(seg, n, bcnt, starts);
+  BS_CUDA(cudaGetLastError());
+  return BS_OK;
+}
+
+}  // extern "C"
+

@@ -157,6 +157,61 @@ def sort_words_device(keys, vals=None, *, width: int, start_pos: int = 0, key_ki
     return status
 
 
+def exact_sort_device(keys, vals=None, *, width: int, start_pos: int = 0, key_kind: int = 0,
+                      mode: int = _lib.EX_REC, passthrough_loop: bool = False, check_after: int = 0,
+                      streak: int = 0, checked: bool = False, par_levels: int = 0, depth: int = 1,
+                      counters=None, on_level=None):
+    """Reference-order sort of a contiguous 1-D CUDA word tensor in place (bs_exact_sort).
+
+    ``mode``: ``_lib.EX_REC`` (kernels.sort_words with its switches),
+    ``EX_ITER`` (sort_words_iterative), ``EX_LEVELS`` (the level observer
+    engine, core._sort_levels) or ``EX_PAR`` (sort_parallel with
+    ``par_levels`` prepartition levels).  ``counters``: CUDA int64[4] that
+    receives the reference counters (overwritten).  ``on_level(pos, starts)``:
+    called after every level with the segment start positions (numpy uint32,
+    ascending) -- syncs the stream once per level.
+    """
+    t = require_cuda()
+    if not keys.is_cuda or keys.dim() != 1 or not keys.is_contiguous():
+        raise ValueError("keys must be a contiguous 1-D CUDA tensor")
+    n = keys.numel()
+    kb = keys.element_size()
+    vb, vptr = 0, None
+    if vals is not None:
+        if not vals.is_cuda or vals.dim() != 1 or not vals.is_contiguous() or vals.numel() != n:
+            raise ValueError("values must be a contiguous 1-D CUDA tensor of the same length")
+        vb, vptr = vals.element_size(), vals.data_ptr()
+    if counters is not None and (counters.dtype != t.int64 or counters.numel() != 4 or not counters.is_cuda):
+        raise ValueError("counters must be a CUDA int64[4] tensor")
+    L = _lib.lib()
+    ws = workspaces.get(L.bs_exact_workspace_bytes(n, kb, vb), keys.device)
+    sptr = stream_ptr(keys.device)
+    cb = None
+    errors = []
+    if on_level is not None:
+        starts = t.empty(max(1, n), dtype=t.int32, device=keys.device)
+        cnt = t.zeros(1, dtype=t.int32, device=keys.device)
+
+        def _level(_ctx, pos):
+            try:
+                _lib.check(L.bs_exact_boundaries(ws.data_ptr(), n, kb, vb, starts.data_ptr(), cnt.data_ptr(), sptr))
+                m = int(cnt.item())
+                on_level(int(pos), starts[:m].cpu().numpy().view(np.uint32))
+            except BaseException as e:  # raised again after the C call returns
+                errors.append(e)
+
+        cb = _lib.LEVEL_FN(_level)
+    with t.cuda.device(keys.device):
+        rc = L.bs_exact_sort(keys.data_ptr(), vptr, n, kb, vb, int(width), int(start_pos), int(key_kind), int(mode),
+                             int(bool(passthrough_loop)), int(check_after), int(streak), int(bool(checked)),
+                             int(par_levels), int(depth), ws.data_ptr(), ws.numel(), sptr,
+                             counters.data_ptr() if counters is not None else None,
+                             cb if cb is not None else _lib.LEVEL_FN(), None)
+    _lib.check(rc)
+    if errors:
+        raise errors[0]
+
+
 def metrics_device(sorted_keys, *, width: int, start_pos: int = 0, key_kind: int = 0, depth: int = 1,
                    counters):
     """Add the closed-form reference Metrics of an already sorted CUDA word tensor."""

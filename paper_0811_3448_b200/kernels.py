@@ -11,11 +11,15 @@ Backend selection mirrors kernels.py:19-35: ``BINARSORT_BACKEND`` must be
 ``auto`` or ``cuda``; anything else raises ``ValueError`` at import.  There
 is no CPU fallback.
 
-Counter exactness: ``partition_words`` counts exactly (closed form of the
-two-cursor loop).  ``sort_words`` with the baseline switches
-(``passthrough_loop=False, check_after=0``) returns the reference counters
-exactly; with the optimisation switches on, the output is
-identical but calls/depth/extractions are those of the baseline recursion.
+Counter exactness: every entry point returns the reference's counters
+exactly.  ``partition_words`` uses the closed form of the two-cursor loop
+(SURVEY Appendix A).  ``sort_words`` with the baseline switches on a
+full-width word range runs the fast digit sort and the closed-form counters
+(Appendix B); every other case -- the optimisation switches, a start bit
+``pos > 0`` or words wider than ``width`` (where the order of equal keys
+shows), and ``sort_words_iterative`` (stack high-water mark) -- runs the exact
+reference-order engine (``bs_exact_sort``, exact_impl.cuh), which replays the
+recursion's partitions level by level.
 """
 
 from __future__ import annotations
@@ -121,23 +125,43 @@ def sort_words(arr, lower, upper, pos, width, passthrough_loop, check_after, str
         return
     r = _Range(arr, lower, upper)
     c = r.t.zeros(4, dtype=r.t.int64, device=r.dev.device)
-    device.sort_words_device(r.dev, width=width, start_pos=pos, key_kind=_lib.BS_KEY_UNSIGNED,
-                             counters=c, depth=depth)
+    baseline = not passthrough_loop and int(check_after) == 0
+    if baseline and int(pos) == 0 and r.dev.element_size() * 8 == int(width):
+        device.sort_words_device(r.dev, width=width, start_pos=pos, key_kind=_lib.BS_KEY_UNSIGNED,
+                                 counters=c, depth=depth)
+    else:
+        device.exact_sort_device(r.dev, width=width, start_pos=pos, key_kind=_lib.BS_KEY_UNSIGNED,
+                                 mode=_lib.EX_REC, passthrough_loop=bool(passthrough_loop),
+                                 check_after=int(check_after), streak=int(streak), checked=bool(checked),
+                                 depth=int(depth), counters=c)
     r.commit()
     _merge_counters(counters, c)
 
 
 def sort_words_iterative(arr, lower, upper, width, counters) -> None:
-    """Explicit-stack form (kernels.py:129-172); identical output."""
+    """Explicit-stack form (kernels.py:129-172): calls = partitions, max_depth = stack high-water."""
     n = int(upper) - int(lower) + 1
     if n < 1:
+        # an empty range is pushed once and passes through every bit (kernels.py:138-160)
+        _bump_calls(counters, int(width), 1)
         return
     r = _Range(arr, lower, upper)
     c = r.t.zeros(4, dtype=r.t.int64, device=r.dev.device)
-    device.sort_words_device(r.dev, width=width, start_pos=0, key_kind=_lib.BS_KEY_UNSIGNED,
-                             counters=c, depth=1)
+    device.exact_sort_device(r.dev, width=width, start_pos=0, key_kind=_lib.BS_KEY_UNSIGNED,
+                             mode=_lib.EX_ITER, counters=c)
     r.commit()
     _merge_counters(counters, c)
+
+
+def _bump_calls(counters, calls, depth):
+    if device.is_torch_tensor(counters):
+        host = counters.cpu().numpy()
+        host[CALLS] += calls
+        host[MAX_DEPTH] = max(int(host[MAX_DEPTH]), int(depth))
+        counters.copy_(device.torch().from_numpy(host))
+    else:
+        counters[CALLS] += calls
+        counters[MAX_DEPTH] = max(int(counters[MAX_DEPTH]), int(depth))
 
 
 def _bump_call(counters, depth):

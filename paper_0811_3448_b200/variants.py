@@ -1,21 +1,32 @@
 """Iterative / optimized / parallel drive forms (drop-in for ``binarsort.variants``).
 
-Reference: ``/root/reference/pkg/src/binarsort/variants.py``.  On the CPU the
-three variants differ in scheduling (explicit stack, pass-through loop and
-sortedness scan, thread-pool over top-bit buckets); all produce the same
-output as the recursive sort (variants.py:1-6).  On B200 there is one
-scheduling -- the level-synchronous device work-list of ``bs_sort``, which
-*is* the iterative form and *is* the bucket-parallel form (every bucket of a
-level is processed concurrently by all 148 SMs) -- so all three route to the
-same CUDA path and return identical output.  Multi-GPU sharding is
-``paper_0811_3448_b200.dist``.
+Reference: ``/root/reference/pkg/src/binarsort/variants.py``.  All three
+produce element-for-element the reference's output AND its counters:
+
+* ``sort_iterative`` -- explicit work stack (variants.py:67-90): calls count
+  partitions, ``max_depth`` is the stack high-water mark;
+* ``sort_optimized`` -- pass-through loop (no call, no depth) and the
+  sortedness scan after a streak of pass-throughs (variants.py:93-121), which
+  inspects the range's current, partially partitioned content;
+* ``sort_parallel`` -- ``ceil(lg workers)`` levels of level-synchronous
+  prepartition, then one recursive sort per bucket from that bit
+  (variants.py:124-229).
+
+On the device they run as modes of the exact reference-order engine
+(``bs_exact_sort``, exact_impl.cuh): every reference call works on a disjoint
+index range, so replaying all ranges of one bit level together reproduces the
+reference's array states, and with them the counters.  The thread pool of
+``sort_parallel`` has no device counterpart -- every bucket of a level is
+processed concurrently by all SMs.  Inputs whose counters need no replay
+(``sort_optimized`` with both switches off) take the fast digit sort;
+multi-GPU sharding is ``paper_0811_3448_b200.dist``.
 """
 
 from __future__ import annotations
 
 from dataclasses import dataclass
 
-from . import core
+from . import _lib, core
 from .core import Metrics
 
 __all__ = ["OptimizationConfig", "sort_iterative", "sort_optimized", "sort_parallel"]
@@ -40,30 +51,51 @@ def _finish(out: Metrics, provided: Metrics | None) -> Metrics:
     return out
 
 
+def _run(seq, codec, **kw) -> Metrics:
+    out = Metrics()
+    n = len(seq)
+    if n <= 1:
+        return out
+    width = codec.width_for(seq)
+    if width == 0:
+        return out
+    core._sort_device(seq, codec, None, width, 0, 1, out, **kw)
+    return out
+
+
 def sort_iterative(seq, codec, metrics: Metrics | None = None) -> Metrics:
-    """Explicit work-list sort (variants.py:67-90); same output as ``core.sort``."""
-    return _finish(core.sort(seq, codec), metrics)
+    """Explicit work-stack sort (variants.py:67-90); max_depth = stack high-water mark."""
+    return _finish(_run(seq, codec, mode=_lib.EX_ITER), metrics)
 
 
 def sort_optimized(seq, codec, config: OptimizationConfig | None = None,
                    metrics: Metrics | None = None) -> Metrics:
-    """Pass-through/sortedness shortcuts (variants.py:93-121).
+    """Pass-through loop and sortedness-scan shortcuts (variants.py:93-121).
 
-    The device sort already skips constant digits (pass-through) and
-    all-equal buckets (sortedness), so the switches change nothing in the
-    output; the returned counters are the baseline recursion's.
+    With both switches off this is the recursive baseline, counters included.
     """
     if config is None:
         config = OptimizationConfig()
-    return _finish(core.sort(seq, codec), metrics)
+    if not config.passthrough_loop and config.sortedness_check_after == 0:
+        return _finish(_run(seq, codec), metrics)
+    return _finish(_run(seq, codec, mode=_lib.EX_REC, passthrough_loop=config.passthrough_loop,
+                        check_after=config.sortedness_check_after), metrics)
 
 
 def sort_parallel(seq, codec, workers: int, metrics: Metrics | None = None) -> Metrics:
     """Bucket-parallel sort (variants.py:162-229); ``workers`` must be >= 1.
 
-    Output identical to the sequential sort.  The GPU processes every bucket
-    of a level concurrently, so ``workers`` only validates.
+    ``levels = min(ceil(lg workers), width)`` prepartition levels, then the
+    recursive sort of every bucket from bit ``levels`` at depth ``levels + 1``
+    -- the reference's partitions and counters.
     """
     if workers < 1:
         raise ValueError("workers must be >= 1")
-    return _finish(core.sort(seq, codec), metrics)
+    n = len(seq)
+    if n <= 1:
+        return _finish(Metrics(), metrics)
+    width = codec.width_for(seq)
+    if width == 0:
+        return _finish(Metrics(), metrics)
+    levels = min((workers - 1).bit_length(), width)
+    return _finish(_run(seq, codec, mode=_lib.EX_PAR, par_levels=levels), metrics)

@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 def test_forced_overflow_is_reported(cuda, cap, vb):
     """Shrunken work lists drop work; bs_sort_status must say so and the shim must raise."""
     t = cuda
-    n = 1 << 20
+    n = 1 << 23  # level-0 children exceed the local-sort size: level-1 buckets, tiles and tasks
     x = mt_words(11, n)
     k = t.from_numpy(x.view(np.int32)).cuda()
     v = t.arange(n, dtype=t.int32, device="cuda") if vb else None
