@@ -374,7 +374,7 @@ def run_gpu(args):
     nev = 1 + 3 * nlev + 1
     import ctypes
 
-    from paper_0811_3448_b200.dist import dist_sort
+    from paper_0811_3448_b200.dist import SAMPLES_PER_RANK, dist_sort
 
     def one_sort(phases=None, marks=None):
         if world > 1:
@@ -503,7 +503,7 @@ def run_gpu(args):
         "clocks": clocks,
         # our kernels per step; N>1: sample, sample sort, class count (4), fused exchange, local sort
         "gpu_launches": (int(L.bs_sort_launches(n, 4, 32, 0, 0)) if world == 1 else
-                         1 + int(L.bs_sort_launches(world * 4096, 4, 32, 0, 0)) + 5 +
+                         1 + int(L.bs_sort_launches(world * SAMPLES_PER_RANK, 4, 32, 0, 0)) + 5 +
                          int(L.bs_sort_launches(n, 4, 32, 0, 0))) * args.steps,
     }
     if world == 1:

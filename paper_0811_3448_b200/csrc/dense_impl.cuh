@@ -67,6 +67,7 @@ struct DenseSmem {
 template <typename K, int KIND, int BLOCK, int CAP, int NSLOT, bool BIG>
 __global__ void __launch_bounds__(BLOCK + 32, BIG ? 1 : 2) dense_kernel(Ws ws, int L) {
   pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
+  if (ws_failed(ws)) return;
   using S = DenseSmem<K, BLOCK, CAP, NSLOT>;
   static_assert(S::NW == 4 * BLOCK, "thread t owns bitmap words 4t..4t+3");
   extern __shared__ __align__(128) unsigned char smem[];

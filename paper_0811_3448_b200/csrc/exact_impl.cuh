@@ -284,9 +284,14 @@ __global__ void __launch_bounds__(256) ex_plan_kernel(Ex e, int L, int pos, int 
       } else if (mode == M_ITER) {  // kernels.py:129-172
         calls += 1;
         uint32_t h;
-        if (last) {
+        if (last) {  // pos + 1 == width: nothing pushed, but the partition still moved the data
           h = P;
-          B[i] = SegT{cnt, pack(stop, 0, 0, P), 0, 0};
+          if (pass) {
+            B[i] = SegT{cnt, pack(stop, 0, 0, P), 0, 0};
+          } else {
+            B[i] = SegT{lo_n, pack(stop, 0, 0, P), 0, 0};
+            B[up_s] = SegT{up_n, pack(stop, 0, 0, P), 0, 0};
+          }
         } else if (pass) {
           h = P + 1u;
           B[i] = SegT{cnt, pack(bits, 0, 0, P), 0, 0};

@@ -128,6 +128,17 @@ struct Ws {
 };
 
 
+// A sort whose work lists overflowed (ctl->error, reported by bs_sort_status)
+// must not consume the entries that were never written: every kernel after
+// init checks the flag once per CTA (block-uniform, before any role split)
+// and exits.
+__device__ __forceinline__ bool ws_failed(const Ws &ws) {
+  __shared__ uint32_t s_fail;
+  if (threadIdx.x == 0) s_fail = *reinterpret_cast<volatile const uint32_t *>(&ws.ctl->error);
+  __syncthreads();
+  return s_fail != 0;
+}
+
 // ---------------------------------------------------------------------------
 // init: root bucket (or a single local task when n fits the local sort).
 // A strided sample guesses the first varying digit so constant leading digits
@@ -196,6 +207,7 @@ __global__ void init_kernel(Ws ws) {
 template <typename K, int KIND, int BLOCK, int KPT>
 __global__ void __launch_bounds__(BLOCK) hist_kernel(Ws ws, int L) {
   pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
+  if (ws_failed(ws)) return;
   constexpr int NCOPY = 4;
   __shared__ uint32_t h[NCOPY][256];
   __shared__ uint64_t s_or[BLOCK / 32], s_and[BLOCK / 32];
@@ -310,6 +322,7 @@ constexpr int H16_MAXCTA = 160;  // >= SM count (one CTA per SM)
 template <typename K, int KIND, int BLOCK>
 __global__ void __launch_bounds__(BLOCK, 1) hist16_kernel(Ws ws) {
   pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
+  if (ws_failed(ws)) return;
   constexpr int W = KeyTraits<K>::BITS;
   constexpr int EPG = 16 / int(sizeof(K));  // keys per 16-byte granule
   constexpr int UNR = 4;                    // granules in flight per thread
@@ -480,6 +493,7 @@ __global__ void __launch_bounds__(BLOCK, 1) hist16_kernel(Ws ws) {
 // rows; the four slices meet in shared memory.  256 threads = 64 quads.
 __global__ void __launch_bounds__(256) hist16_reduce_kernel(Ws ws, int nparts) {
   pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
+  if (ws_failed(ws)) return;
   __shared__ uint4 s_part[3][64][2];  // slices 1..3: (lo sums, hi sums) of 4 words
   if (ws.ctl->nbuckets[0] == 0) return;
   const int tid = threadIdx.x, ql = tid & 63, k = tid >> 6;
@@ -565,6 +579,7 @@ __device__ __forceinline__ void push_bucket(const Ws &ws, int L, uint64_t start,
 template <typename K>
 __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
   pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
+  if (ws_failed(ws)) return;
   constexpr int W = KeyTraits<K>::BITS;
   __shared__ uint32_t s_cnt[256];
   __shared__ uint32_t s_scan[16];
@@ -754,6 +769,7 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
 // map its tiles (tile -> bucket).  One warp per bucket.
 __global__ void __launch_bounds__(256) expand_kernel(Ws ws, int L) {
   pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
+  if (ws_failed(ws)) return;
   const int cur = L & 1;
   const uint32_t nb = min(ws.ctl->nbuckets[L], ws.maxb);
   const int lane = threadIdx.x & 31;
@@ -989,6 +1005,7 @@ constexpr int TS_T = 32;  // tiles per tile_scan block
 
 __global__ void __launch_bounds__(256) tile_scan_kernel(Ws ws, int L) {
   pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
+  if (ws_failed(ws)) return;
   __shared__ uint32_t s_blk;
   __shared__ uint32_t s_b[TS_T], s_start[TS_T];  // tile's bucket; tile starts its bucket
   const int d = threadIdx.x;
@@ -1069,6 +1086,7 @@ struct ScatterSmem {
 template <typename K, int VB, int KIND, int BLOCK, int KPT>
 __global__ void __launch_bounds__(BLOCK, (sizeof(K) + VB) <= 8 ? 3 : 1) scatter_kernel(Ws ws, int L) {
   pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
+  if (ws_failed(ws)) return;
   using S = ScatterSmem<K, VB, KIND, BLOCK, KPT>;
   using D = typename S::D;
   using V = typename S::V;
@@ -1326,6 +1344,7 @@ __device__ __forceinline__ uint32_t scan256_excl_nb(uint32_t v, uint32_t *scratc
 template <typename K, int KIND, int BLOCK, int KPT, int NBUF>
 __global__ void __launch_bounds__(BLOCK + 32, BLOCK >= 512 ? 2 : 3) scatter_ws_kernel(Ws ws, int L) {
   pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
+  if (ws_failed(ws)) return;
   using S = ScatterWsSmem<K, KIND, BLOCK, KPT, NBUF>;
   constexpr int TILE = S::TILE;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -1518,6 +1537,7 @@ struct LocalSmem {
 template <typename K, int VB, int KIND, int BLOCK, int KPT>
 __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
   pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
+  if (ws_failed(ws)) return;
   using S = LocalSmem<K, VB, KIND, BLOCK, KPT>;
   using D = typename S::D;
   using V = typename S::V;

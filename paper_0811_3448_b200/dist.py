@@ -390,6 +390,11 @@ def _host_barrier(group, dev) -> None:
         dist.barrier(group=group)
 
 
+# Splitter samples per rank: the destination loads deviate from N/R by about
+# sqrt(R / (4 * S)) of N/R per boundary, so 65536 keeps them within ~0.5 %
+# at R = 8 (4096 gave ~2-4 % on cfg5); sorting R*S samples costs ~0.1 ms.
+SAMPLES_PER_RANK = 65536
+
 MAX_RANKS = 8  # the split kernels classify into 2R-1 <= 15 classes (16-wide tile rows)
 
 
@@ -409,7 +414,7 @@ def _single_node(group, R: int) -> bool:
 
 
 def dist_sort(keys, values=None, *, width: int, key_kind: int = _lib.BS_KEY_UNSIGNED, ops=None, group=None,
-              samples_per_rank: int = 4096, exchange: str = "auto", marks: list | None = None) -> DistResult:
+              samples_per_rank: int = SAMPLES_PER_RANK, exchange: str = "auto", marks: list | None = None) -> DistResult:
     """Globally sort the shards held by all ranks of ``group``.
 
     ``keys`` (and ``values``) are this rank's contiguous 1-D tensors (CUDA for
