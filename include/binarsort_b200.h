@@ -45,6 +45,9 @@ extern "C" {
 /* Library version (major*10000 + minor*100 + patch). */
 int bs_version(void);
 
+/* 1 in the bounds-checked build (libbinarsort_b200_debug.so), else 0. */
+int bs_debug_checks(void);
+
 /* Thread-local message for the last non-BS_OK return on this thread. */
 const char *bs_last_error(void);
 
@@ -61,7 +64,9 @@ size_t bs_workspace_bytes(uint64_t n, int key_bytes, int val_bytes);
  * bs_sort_from): enqueues on `stream` a 4-byte copy of the sort's overflow
  * flag into *status (device or pinned host memory).  0 = OK; otherwise bit 0
  * bucket-list overflow, bit 1 tile-map overflow, bit 2 task-list overflow --
- * work was dropped and the output is NOT sorted.  The capacities are sized so
+ * work was dropped and the output is NOT sorted -- and, in the bounds-checked
+ * build (libbinarsort_b200_debug.so, -DBS_DEBUG_CHECKS), bit 3 = a write
+ * index failed its check.  The capacities are sized so
  * this cannot happen for any input (Geometry in binarsort_b200.cu); the flag
  * is the loud failure path that proves it (the Python shim raises
  * RuntimeError).  No reference counterpart: the numba kernels cannot run out

@@ -39,31 +39,43 @@ EXPORTS = (
     "bs_sort_from_workspace_bytes", "bs_sort_from", "bs_split_count", "bs_split_exchange",
     "bs_ipc_handle_bytes", "bs_ipc_alloc", "bs_ipc_open", "bs_ipc_close", "bs_ipc_free",
     "bs_sort_status", "bs_debug_capacity", "bs_exact_workspace_bytes", "bs_exact_sort",
-    "bs_exact_boundaries",
+    "bs_exact_boundaries", "bs_debug_checks",
 )
 
 
-def _stale() -> bool:
-    if not os.path.exists(SO_PATH):
+SO_DEBUG_PATH = os.path.join(_HERE, "libbinarsort_b200_debug.so")  # -DBS_DEBUG_CHECKS build
+
+
+def _stale(path: str) -> bool:
+    if not os.path.exists(path):
         return True
-    so_m = os.path.getmtime(SO_PATH)
+    so_m = os.path.getmtime(path)
     deps = [os.path.join(_CSRC, d) for d in _DEPS]
     deps.append(os.path.join(_ROOT, "include", "binarsort_b200.h"))
     return any(os.path.exists(d) and os.path.getmtime(d) > so_m for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile the CUDA library in-tree for sm_100a (no GPU needed)."""
-    if force or _stale():
-        nvcc = os.environ.get("NVCC", "nvcc")
-        if not os.path.isabs(nvcc) and os.path.exists("/usr/local/cuda/bin/nvcc"):
-            nvcc = "/usr/local/cuda/bin/nvcc"
-        tmp = SO_PATH + ".tmp"
-        cmd = [nvcc, *NVCC_FLAGS, "-o", tmp, *[os.path.join(_CSRC, s) for s in _SOURCES]]
-        if verbose:
-            print(" ".join(cmd))
-        subprocess.run(cmd, check=True)
-        os.replace(tmp, SO_PATH)
+def build(force: bool = False, verbose: bool = False, debug: bool = True) -> str:
+    """Compile the CUDA library in-tree for sm_100a (no GPU needed).
+
+    Also builds the bounds-checked variant (``-DBS_DEBUG_CHECKS``) that the
+    test suite runs its parity corpus against (``BS_LIBRARY=debug``).
+    """
+    nvcc = os.environ.get("NVCC", "nvcc")
+    if not os.path.isabs(nvcc) and os.path.exists("/usr/local/cuda/bin/nvcc"):
+        nvcc = "/usr/local/cuda/bin/nvcc"
+    jobs = [(SO_PATH, [])] + ([(SO_DEBUG_PATH, ["-DBS_DEBUG_CHECKS"])] if debug else [])
+    procs = []
+    for path, extra in jobs:
+        if force or _stale(path):
+            cmd = [nvcc, *NVCC_FLAGS, *extra, "-o", path + ".tmp", *[os.path.join(_CSRC, s) for s in _SOURCES]]
+            if verbose:
+                print(" ".join(cmd))
+            procs.append((path, subprocess.Popen(cmd)))
+    for path, p in procs:
+        if p.wait() != 0:
+            raise subprocess.CalledProcessError(p.returncode, "nvcc")
+        os.replace(path + ".tmp", path)
     return SO_PATH
 
 
@@ -79,13 +91,15 @@ def lib() -> ctypes.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        if not os.path.exists(SO_PATH):
+        path = SO_DEBUG_PATH if os.environ.get("BS_LIBRARY", "") == "debug" else SO_PATH
+        if not os.path.exists(path):
             raise RuntimeError(
-                f"{SO_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+                f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
                 " (there is no CPU fallback)")
-        L = ctypes.CDLL(SO_PATH)
+        L = ctypes.CDLL(path)
         vp, u64, i32, i64, sz = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_int64, ctypes.c_size_t
         L.bs_version.restype = i32
+        L.bs_debug_checks.restype = i32
         L.bs_last_error.restype = ctypes.c_char_p
         L.bs_workspace_bytes.argtypes = [u64, i32, i32]
         L.bs_workspace_bytes.restype = sz

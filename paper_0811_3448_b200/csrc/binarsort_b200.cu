@@ -349,7 +349,15 @@ using namespace bs;
 
 extern "C" {
 
-int bs_version(void) { return 100; }
+int bs_version(void) { return 200; }
+
+int bs_debug_checks(void) {
+#ifdef BS_DEBUG_CHECKS
+  return 1;
+#else
+  return 0;
+#endif
+}
 
 const char *bs_last_error(void) { return g_err.c_str(); }
 

@@ -18,6 +18,21 @@ namespace bs {
 
 constexpr int WARP = 32;
 
+// Debug build (-DBS_DEBUG_CHECKS, libbinarsort_b200_debug.so): every global
+// and staging write of the sort kernels checks its index; a violation sets bit
+// 3 of the sort's status word (bs_sort_status) instead of trapping, so the
+// test suite can run the whole parity corpus against the checked build.
+#ifdef BS_DEBUG_CHECKS
+#define BS_DCHECK(ctl, cond)                                   \
+  do {                                                         \
+    if (!(cond)) atomicOr(&(ctl)->error, 8u);                  \
+  } while (0)
+#else
+#define BS_DCHECK(ctl, cond) \
+  do {                       \
+  } while (0)
+#endif
+
 template <int VB> struct ValT { using T = uint32_t; };
 template <> struct ValT<8> { using T = uint64_t; };
 

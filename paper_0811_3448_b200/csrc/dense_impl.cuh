@@ -287,6 +287,7 @@ __global__ void __launch_bounds__(BLOCK + 32, BIG ? 1 : 2) dense_kernel(Ws ws, i
       // from its end (FLO yields the bit index directly).  A second copy is a
       // predicated store; words with third or later copies (rare) take the
       // general loop.
+      BS_DCHECK(ws.ctl, pos + c <= uint32_t(n));
       K *pe = stg + (pos + c);
       const uint32_t w1[4] = {b1.x, b1.y, b1.z, b1.w};
       const uint32_t w2[4] = {b2.x, b2.y, b2.z, b2.w};
@@ -345,6 +346,7 @@ __global__ void __launch_bounds__(BLOCK + 32, BIG ? 1 : 2) dense_kernel(Ws ws, i
     fence_proxy_async_smem();  // staging writes -> visible to the bulk copy
     named_sync<BLOCK>();       // S3
     // ---- store: 16-byte-aligned middle by one bulk copy, ragged ends by threads ----
+    BS_DCHECK(ws.ctl, f.start + uint64_t(n) <= ws.n && n <= CAP);
     {
       const int h = min(n, mis ? int((16u - mis) / sizeof(K)) : 0);
       const int m = ((n - h) / EPG) * EPG;

@@ -1271,6 +1271,7 @@ __global__ void __launch_bounds__(BLOCK, (sizeof(K) + VB) <= 8 ? 3 : 1) scatter_
         const int e = j * BLOCK + tid;
         const K k = kb[e];
         const uint32_t o = gb[dfn(k)] + uint32_t(e);
+        BS_DCHECK(ws.ctl, o < ws.n);
         __stcs(dst + o, k);
         if constexpr (VB != 0) __stcs(vdst + o, vbp[e]);
       }
@@ -1278,6 +1279,7 @@ __global__ void __launch_bounds__(BLOCK, (sizeof(K) + VB) <= 8 ? 3 : 1) scatter_
       for (int e = tid; e < cnt; e += BLOCK) {
         const K k = kb[e];
         const uint32_t o = gb[dfn(k)] + uint32_t(e);
+        BS_DCHECK(ws.ctl, o < ws.n);
         __stcs(dst + o, k);
         if constexpr (VB != 0) __stcs(vdst + o, vbp[e]);
       }
@@ -1472,11 +1474,17 @@ __global__ void __launch_bounds__(BLOCK + 32, BLOCK >= 512 ? 2 : 3) scatter_ws_k
       named_sync<BLOCK>();
       if (fullt) {
 #pragma unroll
-        for (int j = 0; j < KPT; ++j) kb[tstart[dfn(x[j])] + rk.get(j)] = x[j];
+        for (int j = 0; j < KPT; ++j) {
+          BS_DCHECK(ws.ctl, tstart[dfn(x[j])] + rk.get(j) < uint32_t(TILE));
+          kb[tstart[dfn(x[j])] + rk.get(j)] = x[j];
+        }
       } else {
 #pragma unroll
         for (int j = 0; j < KPT; ++j)
-          if (j * BLOCK + tid < cnt) kb[tstart[dfn(x[j])] + rk.get(j)] = x[j];
+          if (j * BLOCK + tid < cnt) {
+            BS_DCHECK(ws.ctl, tstart[dfn(x[j])] + rk.get(j) < uint32_t(cnt));
+            kb[tstart[dfn(x[j])] + rk.get(j)] = x[j];
+          }
       }
       named_sync<BLOCK>();
       K *dst = static_cast<K *>(ws.keys[f.parity ^ 1]);
@@ -1485,11 +1493,13 @@ __global__ void __launch_bounds__(BLOCK + 32, BLOCK >= 512 ? 2 : 3) scatter_ws_k
         for (int j = 0; j < KPT; ++j) {
           const int e = j * BLOCK + tid;
           const K k = kb[e];
+          BS_DCHECK(ws.ctl, gbase[dfn(k)] + uint32_t(e) < ws.n);
           __stcs(dst + (gbase[dfn(k)] + uint32_t(e)), k);
         }
       } else {
         for (int e = tid; e < cnt; e += BLOCK) {
           const K k = kb[e];
+          BS_DCHECK(ws.ctl, gbase[dfn(k)] + uint32_t(e) < ws.n);
           __stcs(dst + (gbase[dfn(k)] + uint32_t(e)), k);
         }
       }
@@ -1912,6 +1922,7 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
           if (32 * j + lane < nvw) {
             const uint32_t d = g.digit(x[j], dig);
             const uint32_t pos = tstart[d] + rk.get(j) + (atomic_pass ? 0u : whist[d]);
+            BS_DCHECK(ws.ctl, pos < uint32_t(n));
             kb[pos] = x[j];
             if constexpr (VB != 0) vbp[pos] = v[j];
           }
@@ -1920,6 +1931,7 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
         first = false;
       }
     }
+    BS_DCHECK(ws.ctl, f.start + uint64_t(n) <= ws.n);
     for (int e = tid; e < n; e += BLOCK) {
       __stcs(dst + e, kb[e]);
       if constexpr (VB != 0) __stcs(vdst + e, vbp[e]);

@@ -102,7 +102,8 @@ def check_status(status) -> None:
     """Raise if a device status word (CUDA int32[1] filled by bs_sort_status) is set (syncs)."""
     v = int(status.item())
     if v:
-        what = [n for b, n in ((1, "bucket list"), (2, "tile map"), (4, "task list")) if v & b]
+        what = [n for b, n in ((1, "bucket list"), (2, "tile map"), (4, "task list"),
+                               (8, "debug-build bounds check")) if v & b]
         raise SortOverflowError(f"device work-list overflow ({', '.join(what)}; status {v}): output is not sorted")
 
 
