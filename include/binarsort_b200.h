@@ -283,6 +283,14 @@ int bs_exact_sort(void *keys, void *vals, uint64_t n, int key_bytes, int val_byt
  */
 int bs_exact_boundaries(const void *ws, uint64_t n, int key_bytes, int val_bytes,
                         uint32_t *starts, uint32_t *count, void *stream);
+/*
+ * The array's current contents after `levels_done` levels -- what the
+ * reference observer reads from the partially sorted sequence between levels
+ * (core.py:175-180; cli.py:160-185 prints them) -- gathered into out_keys
+ * (device, n words).  Call from on_level with the same keys/ws/n/widths.
+ */
+int bs_exact_snapshot(const void *keys, const void *ws, uint64_t n, int key_bytes, int val_bytes,
+                      int levels_done, void *out_keys, void *stream);
 
 #ifdef __cplusplus
 }

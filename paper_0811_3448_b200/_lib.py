@@ -39,7 +39,7 @@ EXPORTS = (
     "bs_sort_from_workspace_bytes", "bs_sort_from", "bs_split_count", "bs_split_exchange",
     "bs_ipc_handle_bytes", "bs_ipc_alloc", "bs_ipc_open", "bs_ipc_close", "bs_ipc_free",
     "bs_sort_status", "bs_debug_capacity", "bs_exact_workspace_bytes", "bs_exact_sort",
-    "bs_exact_boundaries", "bs_debug_checks",
+    "bs_exact_boundaries", "bs_debug_checks", "bs_exact_snapshot",
 )
 
 
@@ -154,6 +154,8 @@ def lib() -> ctypes.CDLL:
         L.bs_exact_sort.restype = i32
         L.bs_exact_boundaries.argtypes = [vp, u64, i32, i32, vp, vp, vp]
         L.bs_exact_boundaries.restype = i32
+        L.bs_exact_snapshot.argtypes = [vp, vp, u64, i32, i32, i32, vp, vp]
+        L.bs_exact_snapshot.restype = i32
         _lib = L
         return L
 

@@ -120,8 +120,8 @@ class DeviceWords:
             dev = device.as_raw_words(src.to("cuda").contiguous())
             src_dtype = src.dtype
 
-            def wb():
-                res = dev.view(src_dtype)
+            def wb(cur=None):
+                res = (dev if cur is None else cur).view(src_dtype)
                 view.copy_(res if res.dtype == view.dtype else res.to(view.dtype))  # D2H straight into view
 
             self._chain(wb)
@@ -139,8 +139,8 @@ class DeviceWords:
             dev = device.to_device_words(host)
             host_dtype = host.dtype
 
-            def wb():
-                out = dev.cpu().numpy().view(host_dtype)
+            def wb(cur=None):
+                out = (dev if cur is None else cur).cpu().numpy().view(host_dtype)
                 view[...] = out if out.dtype == view.dtype else out.astype(view.dtype)
 
             self._chain(wb)
@@ -156,8 +156,8 @@ class DeviceWords:
             negative = (not want_float) and any(int(v) < 0 for v in items)
             dev = device.to_device_words(host)
 
-            def wb():
-                out = dev.cpu().numpy().view(host.dtype)
+            def wb(cur=None):
+                out = (dev if cur is None else cur).cpu().numpy().view(host.dtype)
                 if want_float:
                     seq[lo:hi] = [float(v) for v in out]
                 elif negative:
@@ -171,10 +171,12 @@ class DeviceWords:
 
     def _chain(self, fn):
         prev = self._writeback
+        if prev is None:  # the first writeback is the keys'
+            self._writeback = self._key_wb = fn
+            return
 
         def both():
-            if prev is not None:
-                prev()
+            prev()
             fn()
 
         self._writeback = both
@@ -182,6 +184,17 @@ class DeviceWords:
     def commit(self):
         if self._writeback is not None:
             self._writeback()
+
+    def show_keys(self, current) -> None:
+        """Write a device word tensor (the keys' current state) into the caller's sequence.
+
+        A CUDA tensor sorted in place needs nothing: its storage is not the
+        engine's ping-pong state, so it is written from ``current`` too."""
+        wb = getattr(self, "_key_wb", None)
+        if wb is not None:
+            wb(current)
+        else:
+            self.keys.copy_(current)
 
 
 # ---------------------------------------------------------------------------
@@ -291,12 +304,14 @@ def _tie_order_observable(w, width: int, start_pos: int) -> bool:
 
 
 def _sort_device(seq, codec, values, width, start_pos, depth, metrics, lower=0, upper=None,
-                 with_metrics=True, exact=None, mode=None, **exact_kw):
+                 with_metrics=True, exact=None, mode=None, _holder=None, **exact_kw):
     if codec.gpu_spec(seq) is None:  # generic-engine element types: out of scope
         raise TypeError(f"{type(codec).__name__} on {type(seq).__name__} has no word view "
                         "(the B200 backend sorts 1-D integer/float arrays, tensors and lists)")
     t = device.require_cuda()
     w = DeviceWords(seq, codec, values, lower=lower, upper=upper)
+    if _holder is not None:
+        _holder["w"] = w
     counters = t.zeros(4, dtype=t.int64, device=w.keys.device) if with_metrics else None
     if exact is None:
         exact = mode is not None or (values is None and _tie_order_observable(w, width, start_pos))
@@ -316,7 +331,12 @@ def _sort_levels_device(seq, codec, width, lower, upper, start_pos, metrics, obs
     """core._sort_levels (core.py:146-180) on the device: the observer sees (pos, [(lo, up), ...])."""
     n = upper - lower + 1
 
-    def on_level(pos, starts):
+    holder = {}
+
+    def on_level(pos, starts, current):
+        w = holder.get("w")
+        if w is not None:  # the observer reads the partially sorted sequence (core.py:175-180)
+            w.show_keys(current)
         ends = np.empty(len(starts), dtype=np.int64)
         ends[:-1] = starts[1:].astype(np.int64) - 1
         if len(starts):
@@ -330,7 +350,7 @@ def _sort_levels_device(seq, codec, width, lower, upper, start_pos, metrics, obs
             observer(pos, [(lower, upper)])
         return
     _sort_device(seq, codec, None, width, start_pos, 1, metrics, lower, upper, mode=_lib.EX_LEVELS,
-                 on_level=on_level)
+                 on_level=on_level, _holder=holder)
 
 
 def sort(seq, codec, values=None, *, with_metrics: bool = True, exact: bool | None = None) -> Metrics:

@@ -957,6 +957,31 @@ int bs_exact_sort(void *keys, void *vals, uint64_t n, int key_bytes, int val_byt
 #undef BS_EX
 }
 
+int bs_exact_snapshot(const void *keys, const void *ws, uint64_t n, int key_bytes, int val_bytes, int levels_done,
+                      void *out_keys, void *stream) {
+  if (!ws || !out_keys || (n > 0 && !keys)) return fail(BS_ERR_VALUE, "keys, ws and out_keys must be non-NULL");
+  if (key_bytes != 4 && key_bytes != 8) return fail(BS_ERR_VALUE, "key_bytes must be 4 or 8");
+  if (n == 0) return BS_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const ExLayout l = ex_layout(n, key_bytes, val_bytes);
+  char *b = static_cast<char *>(const_cast<void *>(ws));
+  ex::Ex e{};
+  e.keys[0] = const_cast<void *>(keys);
+  e.keys[1] = b + l.copy;
+  e.seg = reinterpret_cast<uint32_t *>(b + l.seg);
+  e.tab[0] = reinterpret_cast<ex::SegT *>(b + l.tab0);
+  e.tab[1] = reinterpret_cast<ex::SegT *>(b + l.tab1);
+  e.n = n;
+  const int cur = levels_done & 1;
+  const unsigned grid = unsigned(min64((n + 255) / 256, uint64_t(num_sms()) * 16));
+  if (key_bytes == 4)
+    ex::ex_snapshot_kernel<uint32_t><<<grid, 256, 0, st>>>(e, cur, uint32_t(cur), static_cast<uint32_t *>(out_keys));
+  else
+    ex::ex_snapshot_kernel<uint64_t><<<grid, 256, 0, st>>>(e, cur, uint32_t(cur), static_cast<uint64_t *>(out_keys));
+  BS_CUDA(cudaGetLastError());
+  return BS_OK;
+}
+
 int bs_exact_boundaries(const void *ws, uint64_t n, int key_bytes, int val_bytes, uint32_t *starts, uint32_t *count,
                         void *stream) {
   if (!ws || !starts || !count) return fail(BS_ERR_VALUE, "ws, starts and count must be non-NULL");

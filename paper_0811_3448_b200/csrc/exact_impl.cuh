@@ -471,6 +471,20 @@ __global__ void ex_finalize_kernel(Ex e, int cur, uint32_t fpar) {
   }
 }
 
+// Observer support: the array as the reference's observer sees it after a
+// level (each element read from the buffer its segment currently lives in).
+template <typename K>
+__global__ void ex_snapshot_kernel(Ex e, int cur, uint32_t apar, K *out) {
+  const SegT *tab = e.tab[cur];
+  const K *k0 = static_cast<const K *>(e.keys[0]);
+  const K *k1 = static_cast<const K *>(e.keys[1]);
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < e.n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t f = tab[e.seg[i]].flags;
+    const uint32_t home = (f & F_ACTIVE) ? apar : ((f & F_HOME) ? 1u : 0u);
+    out[i] = home ? k1[i] : k0[i];
+  }
+}
+
 // Observer support: the current segments' start positions, in order.
 __global__ void __launch_bounds__(EX_BLOCK) ex_starts_count_kernel(const uint32_t *seg, uint64_t n, uint32_t *bcnt) {
   __shared__ uint32_t sw[EX_BLOCK / 32];

@@ -168,9 +168,9 @@ def exact_sort_device(keys, vals=None, *, width: int, start_pos: int = 0, key_ki
     ``EX_ITER`` (sort_words_iterative), ``EX_LEVELS`` (the level observer
     engine, core._sort_levels) or ``EX_PAR`` (sort_parallel with
     ``par_levels`` prepartition levels).  ``counters``: CUDA int64[4] that
-    receives the reference counters (overwritten).  ``on_level(pos, starts)``:
-    called after every level with the segment start positions (numpy uint32,
-    ascending) -- syncs the stream once per level.
+    receives the reference counters (overwritten).  ``on_level(pos, starts, current)``: called after every level with the
+    segment start positions (numpy uint32, ascending) and the array's current
+    contents (a CUDA word tensor) -- syncs the stream once per level.
     """
     t = require_cuda()
     if not keys.is_cuda or keys.dim() != 1 or not keys.is_contiguous():
@@ -192,12 +192,15 @@ def exact_sort_device(keys, vals=None, *, width: int, start_pos: int = 0, key_ki
     if on_level is not None:
         starts = t.empty(max(1, n), dtype=t.int32, device=keys.device)
         cnt = t.zeros(1, dtype=t.int32, device=keys.device)
+        snap = t.empty_like(keys)
 
         def _level(_ctx, pos):
             try:
                 _lib.check(L.bs_exact_boundaries(ws.data_ptr(), n, kb, vb, starts.data_ptr(), cnt.data_ptr(), sptr))
+                _lib.check(L.bs_exact_snapshot(keys.data_ptr(), ws.data_ptr(), n, kb, vb, int(pos) - int(start_pos) + 1,
+                                               snap.data_ptr(), sptr))
                 m = int(cnt.item())
-                on_level(int(pos), starts[:m].cpu().numpy().view(np.uint32))
+                on_level(int(pos), starts[:m].cpu().numpy().view(np.uint32), snap)
             except BaseException as e:  # raised again after the C call returns
                 errors.append(e)
 
