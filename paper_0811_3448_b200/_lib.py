@@ -17,8 +17,7 @@ _ROOT = os.path.dirname(_HERE)
 SO_PATH = os.path.join(_HERE, "libbinarsort_b200.so")
 _CSRC = os.path.join(_HERE, "csrc")
 _SOURCES = ["binarsort_b200.cu"]
-_DEPS = ["binarsort_b200.cu", "common.cuh", "sort_impl.cuh", "dense_impl.cuh", "metrics_impl.cuh", "misc_impl.cuh",
-         "exact_impl.cuh"]
+_DEPS = sorted(f for f in os.listdir(_CSRC) if f.endswith((".cu", ".cuh"))) if os.path.isdir(_CSRC) else []
 
 BS_OK, BS_ERR_VALUE, BS_ERR_ASSERT, BS_ERR_CUDA, BS_ERR_WORKSPACE, BS_ERR_INTERNAL = range(6)
 BS_KEY_UNSIGNED, BS_KEY_SIGNED, BS_KEY_FLOAT = 0, 1, 2

@@ -15,6 +15,7 @@
 #include "sort_impl.cuh"
 #include "dense_impl.cuh"
 #include "exact_impl.cuh"
+#include "spread_impl.cuh"
 
 namespace bs {
 
@@ -130,8 +131,8 @@ static Geometry geometry(uint64_t n, int kb, int vb, int width_eff) {
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t ctl, buckets[2], bhist[2], bor[2], band[2], tile_bucket[2], status, toff, hist16, h16part, tasks, dtasks, keys, vals,
-      total;
+  size_t ctl, buckets[2], bhist[2], bor[2], band[2], tile_bucket[2], status, toff, hist16, h16part, tasks, tasks2, dtasks,
+      keys, vals, total;
 };
 
 static Layout layout(const Geometry &g, bool own_copy = true) {
@@ -155,6 +156,7 @@ static Layout layout(const Geometry &g, bool own_copy = true) {
   l.hist16 = take(sizeof(uint32_t) * 65536);
   l.h16part = take(sizeof(uint32_t) * 32768 * size_t(H16_MAXCTA));
   l.tasks = take(sizeof(Task) * g.maxtasks);
+  l.tasks2 = take(g.vb == 0 && g.kb == 8 ? sizeof(Task) * g.maxtasks : 0);
   l.dtasks = take(g.vb == 0 ? sizeof(DTask) * g.maxtasks : 0);
   // the ping-pong copy (bs_sort_from uses the caller's source buffer instead)
   l.keys = take(own_copy ? size_t(g.kb) * g.n : 0);
@@ -198,6 +200,7 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   ws.hist16 = reinterpret_cast<uint32_t *>(base + lay.hist16);
   ws.h16part = reinterpret_cast<uint32_t *>(base + lay.h16part);
   ws.tasks = reinterpret_cast<Task *>(base + lay.tasks);
+  ws.tasks2 = reinterpret_cast<Task *>(base + lay.tasks2);
   ws.dtasks = reinterpret_cast<DTask *>(base + lay.dtasks);
   ws.keys[0] = keys;
   ws.keys[1] = src_keys ? src_keys : base + lay.keys;
@@ -238,19 +241,25 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   ws.dense_max = DN_CAP;
   ws.dense_big_max = sizeof(K) == 4 ? DB_CAP : 0;
   auto lc = local_kernel<K, VB, KIND, LC_BLOCK, LC_KPT>;
+  // keys-only 64-bit: spread tasks go to spread_kernel first (1024 x 8 = local_max)
+  constexpr bool SPREAD = VB == 0 && sizeof(K) == 8;
+  constexpr int SP_BLOCK = 1024, SP_KPT = 8;
+  static_assert(!SPREAD || SP_BLOCK * SP_KPT == LC_BLOCK * LC_KPT, "spread tasks are local tasks");
+  using SPS = SpreadSmem<K, SP_BLOCK, SP_KPT>;
+  auto sp = spread_kernel<K, KIND, SP_BLOCK, SP_KPT>;
   auto hk = hist_kernel<K, KIND, HI_BLOCK, HKPT>;
   constexpr int H16_BLOCK = 1024;
   constexpr size_t H16_SMEM = 32768 * sizeof(uint32_t);
   auto h16 = hist16_kernel<K, KIND, H16_BLOCK>;
   struct Setup {
-    int sc_grid, lc_grid, hk_grid, dk_grid, db_grid;
+    int sc_grid, lc_grid, hk_grid, dk_grid, db_grid, sp_grid;
     cudaError_t attr_err;
   };
   static Setup setup[MAX_DEV];
   static std::once_flag once[MAX_DEV];
   const int dev = current_device();
   int &sc_grid = setup[dev].sc_grid, &lc_grid = setup[dev].lc_grid, &hk_grid = setup[dev].hk_grid,
-      &dk_grid = setup[dev].dk_grid, &db_grid = setup[dev].db_grid;
+      &dk_grid = setup[dev].dk_grid, &db_grid = setup[dev].db_grid, &sp_grid = setup[dev].sp_grid;
   cudaError_t &attr_err = setup[dev].attr_err;
   std::call_once(once[dev], [&] {
     cudaError_t e1 = cudaFuncSetAttribute(sc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SS::bytes));
@@ -269,6 +278,9 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
     hk_grid = num_sms() * max_active(hk, HI_BLOCK, 0);
     if (attr_err == cudaSuccess)
       attr_err = cudaFuncSetAttribute(h16, cudaFuncAttributeMaxDynamicSharedMemorySize, int(H16_SMEM));
+    if (SPREAD && attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(sp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(SPS::bytes));
+    sp_grid = SPREAD ? num_sms() * max_active(sp, SP_BLOCK, SPS::bytes) : 0;
   });
   if (attr_err != cudaSuccess) return fail(BS_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
 
@@ -309,7 +321,12 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   if constexpr (VB == 0) {
     if (ws.dense) BS_CUDA(pdl_launch(dk, dk_grid, DN_BLOCK + 32, DS::bytes, st, ws, 0));
   }
-  BS_CUDA(pdl_launch(lc, lc_grid, LC_BLOCK, LS::bytes, st, ws));
+  if constexpr (SPREAD) {
+    BS_CUDA(pdl_launch(sp, sp_grid, SP_BLOCK, SPS::bytes, st, ws));
+    BS_CUDA(pdl_launch(lc, lc_grid, LC_BLOCK, LS::bytes, st, ws, 1));
+  } else {
+    BS_CUDA(pdl_launch(lc, lc_grid, LC_BLOCK, LS::bytes, st, ws, 0));
+  }
   mark(st);
   BS_CUDA(cudaGetLastError());
   return BS_OK;
@@ -482,7 +499,7 @@ int bs_sort_launches(uint64_t n, int key_bytes, int width, int start_pos, int wi
   const int width_eff = width - start_pos;
   if (n <= 1 || width_eff <= 0) return 0;
   const Geometry g = geometry(n, key_bytes, 0, width_eff);
-  int k = 3;  // init + dense + local
+  int k = 3 + (key_bytes == 8 ? 1 : 0);  // init + dense + local (+ spread for 64-bit keys)
   // per level hist/plan/scatter/expand (+ big dense), + the level-0 hist16 reduce
   if (n > g.local_max) k += 4 * (g.ndig + 1) + (key_bytes == 4 ? g.ndig : 0) + 1;
   if (with_counters) k += 2;

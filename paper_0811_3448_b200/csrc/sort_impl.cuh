@@ -94,6 +94,7 @@ struct Ctl {
   uint32_t ndtasks_big;  // big dense tasks (back of dtasks)
   uint32_t dbig_end[MAXLEV + 1];  // ndtasks_big after plan(L) (snapshot by scatter(L))
   uint32_t h16_bad;  // hist16 unusable (the root's digit is the last one)
+  uint32_t ntasks2;  // tasks the spread local sort hands to local_kernel (tasks2)
 };
 
 // Workspace view (all device pointers), built on the host.
@@ -109,6 +110,7 @@ struct Ws {
   uint32_t *hist16;  // [65536]: root histogram of the digit pair (dig, dig+1)
   uint32_t *h16part; // [H16_MAXCTA][32768]: per-CTA packed partial rows
   Task *tasks;
+  Task *tasks2;  // spread_kernel's leftovers for local_kernel (u64 keys-only sorts)
   DTask *dtasks;
   int dense;           // keys-only full-width: dense tasks go to dense_kernel
   uint32_t dense_max;      // small dense_kernel capacity
@@ -1545,7 +1547,7 @@ struct LocalSmem {
 };
 
 template <typename K, int VB, int KIND, int BLOCK, int KPT>
-__global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
+__global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws, int list) {
   pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
   if (ws_failed(ws)) return;
   using S = LocalSmem<K, VB, KIND, BLOCK, KPT>;
@@ -1561,7 +1563,9 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + S::bars_off);
   InFlight *info = reinterpret_cast<InFlight *>(smem + S::info_off);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const uint32_t ntasks = min(ws.ctl->ntasks, ws.maxtasks);
+  // list 0: the task list; list 1: the tasks spread_kernel handed over
+  const Task *tasks = list ? ws.tasks2 : ws.tasks;
+  const uint32_t ntasks = min(list ? ws.ctl->ntasks2 : ws.ctl->ntasks, ws.maxtasks);
   if (blockIdx.x >= ntasks) return;
   const KeyGeom<K, KIND> g{ws.shift0};
   uint32_t *whist = whist_all + w * 256;
@@ -1571,7 +1575,7 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws) {
     f.idx = ti;
     f.valid = 0;
     if (ti < ntasks) {
-      const Task tk = ws.tasks[ti];
+      const Task tk = tasks[ti];
       f.start = tk.start;
       f.cnt = tk.count;
       f.parity = tk.parity;
