@@ -95,6 +95,7 @@ struct Ctl {
   uint32_t dbig_end[MAXLEV + 1];  // ndtasks_big after plan(L) (snapshot by scatter(L))
   uint32_t h16_bad;  // hist16 unusable (the root's digit is the last one)
   uint32_t ntasks2;  // tasks the spread local sort hands to local_kernel (tasks2)
+  uint32_t skewed;   // a root digit holds > 1/16 of the keys (duplicate-heavy data: Zipf)
 };
 
 // Workspace view (all device pointers), built on the host.
@@ -594,6 +595,9 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
     const Bucket bk = ws.buckets[cur][b];
     uint32_t *hist = ws.bhist[cur] + size_t(b) * 256;
     const uint32_t c = hist[tid];
+    // duplicate-heavy input (one root digit with > 1/16 of the keys): 64-bit
+    // local tasks skip the dense-prefix sort, which would mostly hand them on
+    if (L == 0 && b == 0 && c > bk.count / 16u) ws.ctl->skewed = 1u;
     const K var = K(ws.bor[cur][b] ^ ws.band[cur][b]);
     const int dig = int(bk.digit);
     if (var == 0) {  // all keys equal: finished; copy home if needed
@@ -1563,7 +1567,9 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws, int list) {
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + S::bars_off);
   InFlight *info = reinterpret_cast<InFlight *>(smem + S::info_off);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  // list 0: the task list; list 1: the tasks spread_kernel handed over
+  // list 0: the task list; list 1: the tasks spread_kernel handed over (all of
+  // them when the input is skewed and spread_kernel stood aside)
+  if (list && ws.ctl->skewed) list = 0;
   const Task *tasks = list ? ws.tasks2 : ws.tasks;
   const uint32_t ntasks = min(list ? ws.ctl->ntasks2 : ws.ctl->ntasks, ws.maxtasks);
   if (blockIdx.x >= ntasks) return;

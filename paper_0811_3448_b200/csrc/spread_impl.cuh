@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(BLOCK, 1) spread_kernel(Ws ws) {
   InFlight *info = reinterpret_cast<InFlight *>(smem + S::info_off);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const uint32_t ntasks = min(ws.ctl->ntasks, ws.maxtasks);
-  if (blockIdx.x >= ntasks) return;
+  if (blockIdx.x >= ntasks || ws.ctl->skewed) return;  // skewed input: local_kernel takes every task
   const KeyGeom<K, KIND> g{ws.shift0};
   auto slot_keys = [&](int sl) { return reinterpret_cast<K *>(smem + S::buf_off + size_t(sl) * S::kbuf); };
   auto load = [&](int sl, uint32_t ti) {  // thread 0: stream task ti into slot sl
