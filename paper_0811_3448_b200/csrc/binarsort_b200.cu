@@ -305,6 +305,8 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
       else BS_CUDA(pdl_launch(hk, hk_grid, HI_BLOCK, 0, st, ws, L));
       mark(st);
       BS_CUDA(pdl_launch(plan_kernel<K>, num_sms() * 4, 256, 0, st, ws, L));
+      if (L == 0 && VB == 0 && ws.dense)  // whole-input counting, when plan(0) chose it
+        BS_CUDA(pdl_launch(gen16_kernel<K, KIND>, num_sms() * 8, 256, 0, st, ws));
       if constexpr (VB != 0) BS_CUDA(pdl_launch(tile_scan_kernel, num_sms() * 8, 256, 0, st, ws, L));
       mark(st);
       if constexpr (WSPEC) BS_CUDA(pdl_launch(sw, sc_grid, SC_BLOCK + 32, SW::bytes, st, ws, L));
@@ -500,8 +502,8 @@ int bs_sort_launches(uint64_t n, int key_bytes, int width, int start_pos, int wi
   if (n <= 1 || width_eff <= 0) return 0;
   const Geometry g = geometry(n, key_bytes, 0, width_eff);
   int k = 3 + (key_bytes == 8 ? 1 : 0);  // init + dense + local (+ spread for 64-bit keys)
-  // per level hist/plan/scatter/expand (+ big dense), + the level-0 hist16 reduce
-  if (n > g.local_max) k += 4 * (g.ndig + 1) + (key_bytes == 4 ? g.ndig : 0) + 1;
+  // per level hist/plan/scatter/expand (+ big dense), + the level-0 hist16 reduce and gen16
+  if (n > g.local_max) k += 4 * (g.ndig + 1) + (key_bytes == 4 ? g.ndig : 0) + 1 + (width_eff == key_bytes * 8 ? 1 : 0);
   if (with_counters) k += 2;
   return k;
 }

@@ -55,7 +55,7 @@ constexpr uint32_t ST_AGG = 1u << 30;
 constexpr uint32_t ST_INCL = 2u << 30;
 constexpr uint32_t ST_MASK = (1u << 30) - 1;
 
-enum : uint32_t { ACT_SCATTER = 0, ACT_SKIP = 1 };
+enum : uint32_t { ACT_SCATTER = 0, ACT_SKIP = 1, ACT_GEN = 2 };
 
 struct Bucket {
   uint64_t start;
@@ -96,6 +96,8 @@ struct Ctl {
   uint32_t h16_bad;  // hist16 unusable (the root's digit is the last one)
   uint32_t ntasks2;  // tasks the spread local sort hands to local_kernel (tasks2)
   uint32_t skewed;   // a root digit holds > 1/16 of the keys (duplicate-heavy data: Zipf)
+  uint32_t gen;      // the output is generated from hist16 (gen16_kernel); gen_shift: its bit offset
+  uint32_t gen_shift;
 };
 
 // Workspace view (all device pointers), built on the host.
@@ -630,6 +632,39 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
         continue;
       }
     }
+    // Whole-input counting (keys only, full-width words): when every varying
+    // bit of the root lies in the hist16 digit pair, the sorted output is a
+    // function of the 65536-bin histogram alone (value v repeated count[v]
+    // times), so no key moves: hist16 becomes its exclusive prefix and
+    // gen16_kernel writes the output (one read pass + one write pass).
+    if (L == 0 && b == 0 && ws.dense && !ws.stable && ws.ctl->h16_bad == 0u) {
+      const int shA = W - 16 - 8 * dig;
+      if ((var & ~(K(0xFFFF) << shA)) == 0) {
+        uint4 *h4 = reinterpret_cast<uint4 *>(ws.hist16) + tid * 64;  // thread t: bins 256t .. 256t+255
+        uint32_t sum = 0;
+        for (int q = 0; q < 64; ++q) {
+          const uint4 v = h4[q];
+          sum += v.x + v.y + v.z + v.w;
+        }
+        uint32_t run = scan256_excl<256>(sum, s_scan);
+        for (int q = 0; q < 64; ++q) {
+          const uint4 v = h4[q];
+          uint4 o;
+          o.x = run, run += v.x;
+          o.y = run, run += v.y;
+          o.z = run, run += v.z;
+          o.w = run, run += v.w;
+          h4[q] = o;
+        }
+        if (tid == 0) {
+          ws.buckets[cur][b].action = ACT_GEN;
+          ws.ctl->gen_shift = uint32_t(shA);
+          ws.ctl->gen = 1u;
+        }
+        __syncthreads();
+        continue;
+      }
+    }
     // scatter this bucket on digit `dig`
     const uint32_t excl = scan256_excl<256>(c, s_scan);
     hist[tid] = excl;  // digit base within the bucket
@@ -949,6 +984,48 @@ __device__ __forceinline__ K denorm(K nk) {
   else if constexpr (KIND == 1) return nk ^ MSB;
   else return (nk & MSB) ? (nk ^ MSB) : ~nk;
 }
+
+// ---------------------------------------------------------------------------
+// gen16: the output of a whole-input counting sort (plan(0) found every
+// varying bit inside the hist16 digit pair and turned hist16 into its
+// exclusive prefix).  A warp writes 512 consecutive output positions, lane l
+// positions base + l + 32i: the value at p is common | v << shift for the v
+// with prefix[v] <= p < prefix[v+1] (one binary search per lane, then a walk).
+// ---------------------------------------------------------------------------
+template <typename K, int KIND>
+__global__ void __launch_bounds__(256) gen16_kernel(Ws ws) {
+  pdl_wait();
+  if (ws_failed(ws)) return;
+  if (ws.ctl->gen == 0u) return;
+  const int sh = int(ws.ctl->gen_shift);
+  const K common = K(ws.band[0][0]) & ~(K(0xFFFF) << sh);
+  const uint32_t *pre = ws.hist16;
+  K *dst = static_cast<K *>(ws.keys[0]);
+  const uint64_t n = ws.n;
+  const int lane = threadIdx.x & 31;
+  const uint64_t nwarps = uint64_t(gridDim.x) * (blockDim.x >> 5);
+  for (uint64_t base = (uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 512; base < n;
+       base += nwarps * 512) {
+    uint64_t p = base + lane;
+    if (p >= n) continue;
+    uint32_t lo = 0, hi = 65535;  // largest v with pre[v] <= p
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi + 1) >> 1;
+      if (uint64_t(pre[mid]) <= p) lo = mid;
+      else hi = mid - 1;
+    }
+    uint32_t v = lo;
+    uint64_t next = v < 65535 ? pre[v + 1] : n;
+    for (int i = 0; i < 16 && p < n; ++i, p += 32) {
+      while (p >= next) {  // walk to the value holding p (empty values skipped)
+        ++v;
+        next = v < 65535 ? pre[v + 1] : n;
+      }
+      __stcs(dst + p, denorm<K, KIND>(common | (K(v) << sh)));
+    }
+  }
+}
+
 
 // Double-buffered input: two (keys[, vals]) buffers filled by TMA bulk copies.
 template <typename K, int VB, int CAP>

@@ -463,3 +463,41 @@ def test_hist16_constant_second_digit(cuda):
     got = x.copy()
     bs.sort(got, UnsignedCodec(32), with_metrics=False)
     assert np.array_equal(got, np.sort(x))
+
+
+# --------------------------------------------------------------------------
+# whole-input counting (gen16): every varying bit inside the hist16 digit pair
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("case", ["u32_low16", "u32_mid16", "u32_top16", "u32_skew", "u64_mid16", "u64_low9",
+                                  "i32_low16", "f64_span", "u32_straddle"])
+def test_whole_input_counting(cuda, case):
+    rng = np.random.default_rng(hash(case) % 2 ** 32)
+    n = (1 << 22) + 12345
+    if case == "u32_low16":
+        x = (rng.integers(0, 1 << 16, n, dtype=np.uint64) | 0xABCD0000).astype(np.uint32)
+    elif case == "u32_mid16":
+        x = ((rng.integers(0, 1 << 16, n, dtype=np.uint64) << 8) | 0x9E000077).astype(np.uint32)
+    elif case == "u32_top16":
+        x = ((rng.integers(0, 1 << 16, n, dtype=np.uint64) << 16) | 0x1234).astype(np.uint32)
+    elif case == "u32_skew":
+        x = rng.integers(0, 1 << 16, n, dtype=np.uint64).astype(np.uint32)
+        x[rng.random(n) < 0.9] = 77
+    elif case == "u64_mid16":
+        x = (rng.integers(0, 1 << 16, n, dtype=np.uint64) << np.uint64(24)) | np.uint64(0x5555000000FFFFFF)
+    elif case == "u64_low9":
+        x = rng.integers(0, 1 << 9, n, dtype=np.uint64) | np.uint64(0xFEDCBA9876540000)
+    elif case == "i32_low16":
+        x = (rng.integers(-(1 << 15), 1 << 15, n)).astype(np.int32)
+    elif case == "f64_span":
+        x = np.frombuffer((rng.integers(0, 1 << 16, n, dtype=np.uint64) << np.uint64(30) |
+                           np.uint64(0x4010000000000000)).tobytes(), dtype=np.float64).copy()
+    else:  # varying bits straddle the pair: the ordinary MSD path
+        x = ((rng.integers(0, 1 << 18, n, dtype=np.uint64) << 7)).astype(np.uint32)
+    codec = {np.dtype(np.uint32): UnsignedCodec(32), np.dtype(np.uint64): UnsignedCodec(64),
+             np.dtype(np.int32): SignedCodec(32), np.dtype(np.float64): Float64Codec()}[x.dtype]
+    a = x.copy()
+    m = bs.sort(a, codec)
+    want = np.sort(x) if x.dtype.kind != "f" else x[np.argsort(x, kind="stable")]
+    assert np.array_equal(a.view(np.uint8), want.view(np.uint8)), case
+    assert m.bit_extractions > 0
