@@ -356,6 +356,7 @@ __global__ void __launch_bounds__(BLOCK, 1) hist16_kernel(Ws ws) {
   const uint4 *gsrc = reinterpret_cast<const uint4 *>(src - head);
   const uint64_t ng = (uint64_t(head) + n + EPG - 1) / EPG;
   const uint64_t g0 = ng * blockIdx.x / gridDim.x, g1 = ng * (blockIdx.x + 1) / gridDim.x;
+  const uint64_t gA = head ? 1u : 0u, gB = (uint64_t(head) + n) / EPG;  // granules [gA, gB) hold only keys
   K o = 0, a = ~K(0);
   // Bin p: count in half (p & 1) of word p >> 1, incremented without a
   // return value.  Epochs of at most 32768 keys per CTA are separated by a
@@ -376,34 +377,49 @@ __global__ void __launch_bounds__(BLOCK, 1) hist16_kernel(Ws ws) {
 #pragma unroll
     for (int u0 = 0; u0 < GPE; u0 += UNR) {
       uint4 v[UNR];
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) {  // a warp's batch: 32*UNR consecutive granules
-        const uint64_t gi = eb + uint64_t(u0) * BLOCK + uint64_t(w) * (32 * UNR) + uint64_t(u) * 32 + lane;
-        v[u] = gi < g1 ? __ldcs(gsrc + gi) : make_uint4(0, 0, 0, 0);
-      }
       K nk[UNR * EPG];
       uint32_t valid = 0;
       K ob = 0, ab = ~K(0);
+      const uint64_t bstart = eb + uint64_t(u0) * BLOCK, bend = bstart + uint64_t(UNR) * BLOCK;
+      if (bstart >= gA && bend <= gB && bend <= g1) {  // block-uniform: every key of the batch is valid
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        const uint64_t gi = eb + uint64_t(u0) * BLOCK + uint64_t(w) * (32 * UNR) + uint64_t(u) * 32 + lane;
-        K kk[EPG];
-        if constexpr (sizeof(K) == 4) {
-          kk[0] = K(v[u].x), kk[1] = K(v[u].y), kk[2 % EPG] = K(v[u].z), kk[3 % EPG] = K(v[u].w);
-        } else {
-          kk[0] = K((uint64_t(v[u].y) << 32) | v[u].x);
-          kk[1 % EPG] = K((uint64_t(v[u].w) << 32) | v[u].z);
-        }
-        const int64_t e0 = int64_t(gi * EPG) - int64_t(head);
-        if (gi < g1 && e0 >= 0 && e0 + EPG <= int64_t(n)) {
-          valid |= ((1u << EPG) - 1u) << (u * EPG);
+        for (int u = 0; u < UNR; ++u)
+          v[u] = __ldcs(gsrc + (bstart + uint64_t(w) * (32 * UNR) + uint64_t(u) * 32 + lane));
+        valid = (1u << (UNR * EPG)) - 1u;
 #pragma unroll
-          for (int j = 0; j < EPG; ++j) {
-            nk[u * EPG + j] = g.norm(kk[j]);
-            ob |= nk[u * EPG + j];
-            ab &= nk[u * EPG + j];
+        for (int u = 0; u < UNR; ++u) {
+          K kk[EPG];
+          if constexpr (sizeof(K) == 4) {
+            kk[0] = K(v[u].x), kk[1] = K(v[u].y), kk[2 % EPG] = K(v[u].z), kk[3 % EPG] = K(v[u].w);
+          } else {
+            kk[0] = K((uint64_t(v[u].y) << 32) | v[u].x);
+            kk[1 % EPG] = K((uint64_t(v[u].w) << 32) | v[u].z);
           }
-        } else {
+#pragma unroll
+          for (int j = 0; j < EPG; ++j) nk[u * EPG + j] = g.norm(kk[j]);
+        }
+#pragma unroll
+        for (int i = 0; i < UNR * EPG; i += 2) {
+          ob |= nk[i] | nk[i + 1];
+          ab &= nk[i] & nk[i + 1];
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {  // a warp's batch: 32*UNR consecutive granules
+          const uint64_t gi = bstart + uint64_t(w) * (32 * UNR) + uint64_t(u) * 32 + lane;
+          v[u] = gi < g1 ? __ldcs(gsrc + gi) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+          const uint64_t gi = bstart + uint64_t(w) * (32 * UNR) + uint64_t(u) * 32 + lane;
+          K kk[EPG];
+          if constexpr (sizeof(K) == 4) {
+            kk[0] = K(v[u].x), kk[1] = K(v[u].y), kk[2 % EPG] = K(v[u].z), kk[3 % EPG] = K(v[u].w);
+          } else {
+            kk[0] = K((uint64_t(v[u].y) << 32) | v[u].x);
+            kk[1 % EPG] = K((uint64_t(v[u].w) << 32) | v[u].z);
+          }
+          const int64_t e0 = int64_t(gi * EPG) - int64_t(head);
 #pragma unroll
           for (int j = 0; j < EPG; ++j) {
             nk[u * EPG + j] = g.norm(kk[j]);
