@@ -73,6 +73,9 @@ size_t bs_workspace_bytes(uint64_t n, int key_bytes, int val_bytes);
  * of work-list space (kernels.py:88-126 recurses on the call stack).
  */
 int bs_sort_status(const void *ws, int32_t *status, void *stream);
+/* Byte offset of that status word inside the workspace: a caller that
+ * synchronises the stream anyway can read it in place (no copy launched). */
+size_t bs_sort_status_offset(void);
 
 /*
  * Test hook: cap the work-list capacities (buckets, tiles, tasks) of the

@@ -38,7 +38,7 @@ EXPORTS = (
     "bs_sort_from_workspace_bytes", "bs_sort_from", "bs_split_count", "bs_split_exchange",
     "bs_ipc_handle_bytes", "bs_ipc_alloc", "bs_ipc_open", "bs_ipc_close", "bs_ipc_free",
     "bs_sort_status", "bs_debug_capacity", "bs_exact_workspace_bytes", "bs_exact_sort",
-    "bs_exact_boundaries", "bs_debug_checks", "bs_exact_snapshot",
+    "bs_exact_boundaries", "bs_debug_checks", "bs_exact_snapshot", "bs_sort_status_offset",
 )
 
 
@@ -144,6 +144,7 @@ def lib() -> ctypes.CDLL:
         L.bs_ipc_free.restype = i32
         L.bs_sort_status.argtypes = [vp, vp, vp]
         L.bs_sort_status.restype = i32
+        L.bs_sort_status_offset.restype = sz
         L.bs_debug_capacity.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32]
         L.bs_debug_capacity.restype = None
         L.bs_exact_workspace_bytes.argtypes = [u64, i32, i32]

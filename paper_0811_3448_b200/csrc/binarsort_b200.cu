@@ -426,6 +426,8 @@ int bs_sort_status(const void *ws, int32_t *status, void *stream) {
   return BS_OK;
 }
 
+size_t bs_sort_status_offset(void) { return offsetof(Ctl, error); }
+
 void bs_debug_capacity(uint32_t max_buckets, uint32_t max_tiles, uint32_t max_tasks) {
   t_cap_b = max_buckets;
   t_cap_t = max_tiles;

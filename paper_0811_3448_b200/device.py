@@ -150,8 +150,10 @@ def sort_words_device(keys, vals=None, *, width: int, start_pos: int = 0, key_ki
         _lib.check(rc)
         if n <= 1 or width - start_pos <= 0:
             return None  # nothing launched
-        status = t.empty(1, dtype=t.int32, device=keys.device)
-        _lib.check(L.bs_sort_status(workspace.data_ptr(), status.data_ptr(), stream_ptr(keys.device)))
+        # the sort's status word, read in place from the workspace (no copy
+        # launched); valid until the workspace's next sort
+        off = int(L.bs_sort_status_offset())
+        status = workspace[off:off + 4].view(t.int32)
     if check:
         check_status(status)
         return None

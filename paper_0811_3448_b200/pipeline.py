@@ -96,6 +96,9 @@ class SortPipeline:
                         else:
                             st = device.sort_words_device(d, width=width, key_kind=self.key_kind, counters=c,
                                                           check=False)
+                            # the status word lives in the sort stream's workspace: read it
+                            # before that stream's next sort resets it
+                            host_st[i:i + 1].copy_(st, non_blocking=True)
                     elif self.with_metrics:
                         self.ctr[j].zero_()
                     self.ev_sorted[j].record(self.s_sort)
@@ -105,9 +108,6 @@ class SortPipeline:
                     dst.view(raw).copy_(d, non_blocking=True)
                     if self.with_metrics:
                         host_ctr[i].copy_(self.ctr[j], non_blocking=True)
-                    if st is not None:
-                        st.record_stream(self.s_out)  # allocated on the sort stream, read here
-                        host_st[i:i + 1].copy_(st, non_blocking=True)
                     ev = t.cuda.Event()
                     ev.record(self.s_out)
                     self.ev_free[j] = ev
