@@ -741,7 +741,7 @@ int bs_split_exchange(const void *keys, const void *vals, uint64_t n, int key_by
                                               static_cast<const K *>(splitters), nsp, w.tile_hist,
                                               reinterpret_cast<const long long *>(delta),
                                               reinterpret_cast<const unsigned long long *>(bounds), nranks,
-                                              reinterpret_cast<K *const *>(dst_keys), dst_vals);
+                                              reinterpret_cast<K *const *>(dst_keys), dst_vals, w.class_base + 32);
     BS_CUDA(cudaGetLastError());
     return BS_OK;
   });

@@ -478,6 +478,7 @@ __global__ void __launch_bounds__(512) split_top_scan_kernel(uint32_t *chunk_sum
   if (lane == 0) tot[c] = run;
   __syncthreads();
   if (threadIdx.x == 0) {
+    class_base[32] = 0u;  // split_exchange_kernel's completion ticket
     uint32_t b = 0;
     for (int k = 0; k < 16; ++k) {
       class_base[k] = b;
@@ -571,7 +572,7 @@ template <typename K, int VB, int KIND>
 __global__ void __launch_bounds__(SPLIT_BLOCK, sizeof(K) + VB <= 4 ? 4 : sizeof(K) + VB <= 8 ? 3 : 2) split_exchange_kernel(
     const K *keys, const void *vals_, uint64_t n, int shift0, const K *spl, int nsp, const uint32_t *tile_off,
     const long long *delta, const unsigned long long *bounds, int nranks, K *const *dst_keys,
-    void *const *dst_vals) {
+    void *const *dst_vals, uint32_t *ticket) {
   using V = typename ValT<VB>::T;
   using S = ExchangeSmem<K, VB>;
   constexpr int NW = SPLIT_BLOCK / 32;
@@ -737,12 +738,16 @@ __global__ void __launch_bounds__(SPLIT_BLOCK, sizeof(K) + VB <= 4 ? 4 : sizeof(
     }
   }
   // The receivers are ordered after this grid by stream order on this GPU
-  // plus a collective (its system-scope release comes later in the stream).
-  // One system fence per CTA, after all of the CTA's stores (cumulative
-  // through the barrier), keeps the ordering explicit without making every
-  // thread wait for its own stores to drain.
+  // plus a collective later in the stream.  Release chain, explicit: every
+  // CTA's stores (cumulative through the barrier) are ordered by a GPU-scope
+  // fence before its ticket; the last CTA to take a ticket has observed all
+  // of them and issues ONE system-scope fence -- instead of a system fence
+  // per CTA, which holds the CTA's SM slot until its peer stores drain.
   __syncthreads();
-  if (tid == 0) __threadfence_system();
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(ticket, 1u) == gridDim.x - 1u) __threadfence_system();
+  }
 }
 
 }  // namespace bs
