@@ -1259,6 +1259,11 @@ __global__ void __launch_bounds__(BLOCK, (sizeof(K) + VB) <= 8 ? 3 : 1) scatter_
       continue;
     }
     BS_PROBE(0);
+    // stable sorts: this tile's precomputed digit-run offsets, loaded now so
+    // the global load overlaps the copy wait and the ranking
+    uint32_t toffv = 0;
+    if constexpr (STABLE)
+      if (tid < 256) toffv = ws.toff[size_t(f.idx) * 256 + tid];
     mbar_wait(&bars[cur], (phase >> cur) & 1u);
     phase ^= 1u << cur;
     BS_PROBE(1);
@@ -1325,7 +1330,7 @@ __global__ void __launch_bounds__(BLOCK, (sizeof(K) + VB) <= 8 ? 3 : 1) scatter_
         // element offset of this tile's digit-d run minus its tile position
         // (tile_scan_kernel: digit base + earlier tiles' digit-d counts;
         // mod 2^32: true offsets are < n <= 2^30)
-        reinterpret_cast<uint32_t *>(gbase)[tid] = bucket_start + ws.toff[size_t(f.idx) * 256 + tid] - texcl;
+        reinterpret_cast<uint32_t *>(gbase)[tid] = bucket_start + toffv - texcl;
       }
     } else {
       // Keys-only MSD: the order of keys inside a child bucket is irrelevant
