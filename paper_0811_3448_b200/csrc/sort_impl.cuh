@@ -569,8 +569,10 @@ struct Emit {
   uint32_t digit;  // the child's digit value, or 0xFFFFFFFF for a group of children
 };
 
+// Task.parity: bit 0 the buffer holding the data, bits 8+ the first digit
+// that may vary inside the task (digits above it are shared by its keys).
 __device__ __forceinline__ void emit_tasks(const Ws &ws, uint64_t start, uint64_t count,
-                                           uint32_t parity) {
+                                           uint32_t parity, uint32_t digit = 0u) {
   // chunks of <= local_max (callers: all-equal ranges that only need a copy,
   // or ranges the local sort takes whole)
   const uint64_t nch = (count + ws.local_max - 1) / ws.local_max;
@@ -581,7 +583,7 @@ __device__ __forceinline__ void emit_tasks(const Ws &ws, uint64_t start, uint64_
   }
   for (uint64_t c = 0; c < nch; ++c) {
     const uint64_t s = c * ws.local_max;
-    ws.tasks[base + c] = Task{start + s, uint32_t(min64(ws.local_max, count - s)), parity};
+    ws.tasks[base + c] = Task{start + s, uint32_t(min64(ws.local_max, count - s)), (parity & 1u) | (digit << 8)};
   }
 }
 
@@ -629,7 +631,7 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
     if (dstar != dig) {  // digit constant here (pass-through): requeue at dstar
       if (tid == 0) {
         ws.buckets[cur][b].action = ACT_SKIP;
-        if (bk.count <= ws.local_max) emit_tasks(ws, bk.start, bk.count, bk.parity);
+        if (bk.count <= ws.local_max) emit_tasks(ws, bk.start, bk.count, bk.parity, uint32_t(dstar));
         else push_bucket(ws, L, bk.start, bk.count, uint32_t(dstar), bk.parity);
       }
       continue;
@@ -641,7 +643,7 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
       if (__syncthreads_count(c != 0u) == 1) {
         if (tid == 0) {
           ws.buckets[cur][b].action = ACT_SKIP;
-          if (bk.count <= ws.local_max) emit_tasks(ws, bk.start, bk.count, bk.parity);
+          if (bk.count <= ws.local_max) emit_tasks(ws, bk.start, bk.count, bk.parity, uint32_t(dig + 1));
           else if (dig + 1 < ws.ndig) push_bucket(ws, L, bk.start, bk.count, uint32_t(dig + 1), bk.parity);
           else if (bk.parity) emit_tasks(ws, bk.start, bk.count, 1);  // every digit constant: all equal
         }
@@ -807,7 +809,8 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
             atomicOr(&ws.ctl->error, 4u);
           }
         } else {
-          emit_tasks(ws, e.start, e.count, cpar);
+          // a group of small children still varies in this digit; a standalone child from the next
+          emit_tasks(ws, e.start, e.count, cpar, e.digit == 0xFFFFFFFFu ? uint32_t(dig) : uint32_t(dig + 1));
         }
       } else {
         const uint32_t nt = uint32_t((e.count + ws.tile - 1) / ws.tile);
@@ -1682,7 +1685,7 @@ __global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws, int list) {
       const Task tk = tasks[ti];
       f.start = tk.start;
       f.cnt = tk.count;
-      f.parity = tk.parity;
+      f.parity = tk.parity & 1u;
       f.valid = 1;
       issue_copy<K, VB, S::CAP>(ws, dbuf, bars, slot, f);
     }

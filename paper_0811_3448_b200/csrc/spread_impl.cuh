@@ -47,14 +47,13 @@ __global__ void __launch_bounds__(BLOCK, 1) spread_kernel(Ws ws) {
   if (ws_failed(ws)) return;
   using S = SpreadSmem<K, BLOCK, KPT>;
   constexpr int W = KeyTraits<K>::BITS;
-  constexpr int NW = BLOCK / 32;
   extern __shared__ __align__(128) unsigned char smem[];
   uint32_t *binw = reinterpret_cast<uint32_t *>(smem + S::bins_off);  // bin p: half (p & 1) of word p >> 1
   uint64_t *red = reinterpret_cast<uint64_t *>(smem + S::red_off);
   uint32_t *misc = reinterpret_cast<uint32_t *>(smem + S::misc_off);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + S::bar_off);
   InFlight *info = reinterpret_cast<InFlight *>(smem + S::info_off);
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int tid = threadIdx.x;
   const uint32_t ntasks = min(ws.ctl->ntasks, ws.maxtasks);
   if (blockIdx.x >= ntasks || ws.ctl->skewed) return;  // skewed input: local_kernel takes every task
   const KeyGeom<K, KIND> g{ws.shift0};
@@ -66,7 +65,8 @@ __global__ void __launch_bounds__(BLOCK, 1) spread_kernel(Ws ws) {
       const Task tk = ws.tasks[ti];
       f.start = tk.start;
       f.cnt = tk.count;
-      f.parity = tk.parity;
+      f.parity = tk.parity & 1u;
+      f.digit = tk.parity >> 8;  // first digit that may vary: the prefix is it and the next one
       const Span sk = span16(static_cast<const K *>(ws.keys[f.parity]) + f.start, f.cnt);
       f.headk = sk.head;
       info[sl] = f;
@@ -97,7 +97,6 @@ __global__ void __launch_bounds__(BLOCK, 1) spread_kernel(Ws ws) {
     // keys in registers: element tid + j*BLOCK (strided: conflict-free)
     K x[KPT];
     uint32_t valid = 0;
-    K o = 0, a = ~K(0);
 #pragma unroll
     for (int j = 0; j < KPT; ++j) {
       if (j * BLOCK >= n) break;  // block-uniform: no work past the task's last key
@@ -106,52 +105,13 @@ __global__ void __launch_bounds__(BLOCK, 1) spread_kernel(Ws ws) {
       if (e < n) {
         x[j] = kb[head + e];
         valid |= 1u << j;
-        const K nk = g.norm(x[j]);
-        o |= nk;
-        a &= nk;
       }
-    }
-    auto redux_or = [](K v) -> K {  // REDUX on 32-bit halves (one instruction each)
-      if constexpr (sizeof(K) == 8)
-        return K((uint64_t(__reduce_or_sync(0xFFFFFFFFu, uint32_t(uint64_t(v) >> 32))) << 32) |
-                 __reduce_or_sync(0xFFFFFFFFu, uint32_t(v)));
-      else
-        return K(__reduce_or_sync(0xFFFFFFFFu, uint32_t(v)));
-    };
-    auto redux_and = [](K v) -> K {
-      if constexpr (sizeof(K) == 8)
-        return K((uint64_t(__reduce_and_sync(0xFFFFFFFFu, uint32_t(uint64_t(v) >> 32))) << 32) |
-                 __reduce_and_sync(0xFFFFFFFFu, uint32_t(v)));
-      else
-        return K(__reduce_and_sync(0xFFFFFFFFu, uint32_t(v)));
-    };
-    o = redux_or(o);
-    a = redux_and(a);
-    if (lane == 0) {
-      red[w] = uint64_t(o);
-      red[NW + w] = uint64_t(a);
-    }
-    __syncthreads();  // every key is in registers; masks per warp
-    K var;
-    {
-      const K oo = redux_or(lane < NW ? K(red[lane]) : K(0));
-      const K aa = redux_and(lane < NW ? K(red[NW + lane]) : ~K(0));
-      var = oo ^ aa;
     }
     K *dst = static_cast<K *>(ws.keys[0]) + f.start;
-    if (var == 0) {  // all equal: already sorted; copy home if it lives in the copy
-      if (f.parity) {
-#pragma unroll
-        for (int j = 0; j < KPT; ++j) {
-          if (j * BLOCK >= n) break;
-          if ((valid >> j) & 1u) dst[tid + j * BLOCK] = x[j];
-        }
-      }
-      continue;
-    }
-    // prefix = the top 16 varying bits of the normalised key
-    const int hb = W - 1 - KeyTraits<K>::clz(var);
-    const int sh = hb + 1 > 16 ? hb + 1 - 16 : 0;
+    // prefix = the task's first two possibly-varying digits (the digits above
+    // them are shared by the task's keys).  If they are constant after all,
+    // every key lands on one prefix and the task is handed on below.
+    const int sh = max(W - 8 * int(f.digit) - 16, 0);
     uint32_t *B1 = binw, *B2 = binw + 2048, *B3 = binw + 4096, *P = binw + 6144;
     for (int i = tid; i < 3 * 2048 / 4; i += BLOCK) reinterpret_cast<uint4 *>(binw)[i] = make_uint4(0, 0, 0, 0);
     if (tid == 0) misc[40] = 0;
