@@ -53,6 +53,7 @@ class SortPipeline:
             self.s_in, self.s_sort, self.s_out = t.cuda.Stream(), t.cuda.Stream(), t.cuda.Stream()
             self.buf = [t.empty(int(capacity), dtype=raw, device=self.dev) for _ in range(self.slots)]
             self.ctr = [t.zeros(4, dtype=t.int64, device=self.dev) for _ in range(self.slots)]
+            self.stw = [t.zeros(1, dtype=t.int32, device=self.dev) for _ in range(self.slots)]
         self.ev_in = [t.cuda.Event() for _ in range(self.slots)]
         self.ev_sorted = [t.cuda.Event() for _ in range(self.slots)]
         self.ev_free = [None] * self.slots
@@ -93,14 +94,18 @@ class SortPipeline:
                         c = self.ctr[j] if self.with_metrics else None
                         if width < self.kb * 8:
                             device.exact_sort_device(d, width=width, key_kind=self.key_kind, counters=c)
+                            self.stw[j].zero_()
                         else:
                             st = device.sort_words_device(d, width=width, key_kind=self.key_kind, counters=c,
                                                           check=False)
-                            # the status word lives in the sort stream's workspace: read it
-                            # before that stream's next sort resets it
-                            host_st[i:i + 1].copy_(st, non_blocking=True)
-                    elif self.with_metrics:
-                        self.ctr[j].zero_()
+                            # the status word lives in the sort stream's workspace: keep it
+                            # with the slot before that stream's next sort resets it (an
+                            # SM-side op: a copy here would queue behind the big D2H copies)
+                            t.add(st, 0, out=self.stw[j])
+                    else:
+                        self.stw[j].zero_()
+                        if self.with_metrics:
+                            self.ctr[j].zero_()
                     self.ev_sorted[j].record(self.s_sort)
                 # 3. copy out: keys, counters and the overflow status
                 with t.cuda.stream(self.s_out):
@@ -108,6 +113,7 @@ class SortPipeline:
                     dst.view(raw).copy_(d, non_blocking=True)
                     if self.with_metrics:
                         host_ctr[i].copy_(self.ctr[j], non_blocking=True)
+                    host_st[i:i + 1].copy_(self.stw[j], non_blocking=True)
                     ev = t.cuda.Event()
                     ev.record(self.s_out)
                     self.ev_free[j] = ev
@@ -128,3 +134,4 @@ class SortPipeline:
     def close(self):
         self.buf = []
         self.ctr = []
+        self.stw = []
