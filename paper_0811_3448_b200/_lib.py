@@ -90,7 +90,9 @@ def lib() -> ctypes.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        path = SO_DEBUG_PATH if os.environ.get("BS_LIBRARY", "") == "debug" else SO_PATH
+        which = os.environ.get("BS_LIBRARY", "")
+        # "debug": the bounds-checked build; a path: a scratch build (kernel experiments)
+        path = SO_DEBUG_PATH if which == "debug" else (which if which.endswith(".so") else SO_PATH)
         if not os.path.exists(path):
             raise RuntimeError(
                 f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"

@@ -232,11 +232,12 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   // dense local sort (bitmap enumeration): 512 consumers, 5632-key tasks,
   // 2-slot ring; big variant (u32 only) 18432-key tasks (e.g. 2^30-key
   // inputs), single slot
-  constexpr int DN_BLOCK = 512, DN_CAP = 5632, DN_SLOTS = 2;
+  constexpr int DN_BLOCK = 512;
+  constexpr int D2_BLOCK = 256, DN_CAP = 4608, DN_SLOTS = 2;
   constexpr int DB_CAP = sizeof(K) == 4 ? 18432 : 6144;
-  using DS = DenseSmem<K, DN_BLOCK, DN_CAP, DN_SLOTS>;
+  using DS = Dense2Smem<K, D2_BLOCK, DN_CAP, DN_SLOTS>;
   using DB = DenseSmem<K, DN_BLOCK, DB_CAP, 1>;
-  auto dk = dense_kernel<K, KIND, DN_BLOCK, DN_CAP, DN_SLOTS, false>;
+  auto dk = dense2_kernel<K, KIND, D2_BLOCK, DN_CAP, DN_SLOTS>;
   auto db = dense_kernel<K, KIND, DN_BLOCK, DB_CAP, 1, true>;
   ws.dense_max = DN_CAP;
   ws.dense_big_max = sizeof(K) == 4 ? DB_CAP : 0;
@@ -271,7 +272,7 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
       e4 = cudaFuncSetAttribute(db, cudaFuncAttributeMaxDynamicSharedMemorySize, int(DB::bytes));
     db_grid = VB == 0 ? num_sms() * max_active(db, DN_BLOCK + 32, DB::bytes) : 0;
     attr_err = e1 != cudaSuccess ? e1 : (e2 != cudaSuccess ? e2 : (e3 != cudaSuccess ? e3 : e4));
-    dk_grid = VB == 0 ? num_sms() * max_active(dk, DN_BLOCK + 32, DS::bytes) : 0;
+    dk_grid = VB == 0 ? num_sms() * max_active(dk, D2_BLOCK + 32, DS::bytes) : 0;
     sc_grid = WSPEC ? num_sms() * max_active(sw, SC_BLOCK + 32, SW::bytes)
                     : num_sms() * max_active(sc, SC_BLOCK, SS::bytes);
     lc_grid = num_sms() * max_active(lc, LC_BLOCK, LS::bytes);
@@ -321,7 +322,7 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
     }
   }
   if constexpr (VB == 0) {
-    if (ws.dense) BS_CUDA(pdl_launch(dk, dk_grid, DN_BLOCK + 32, DS::bytes, st, ws, 0));
+    if (ws.dense) BS_CUDA(pdl_launch(dk, dk_grid, D2_BLOCK + 32, DS::bytes, st, ws));
   }
   if constexpr (SPREAD) {
     BS_CUDA(pdl_launch(sp, sp_grid, SP_BLOCK, SPS::bytes, st, ws));

@@ -276,7 +276,11 @@ __global__ void __launch_bounds__(BLOCK) hist_kernel(Ws ws, int L) {
     // clear this tile's look-back row (256 x u32 = 64 x uint4)
     if (ws.stable && tid < 64)
       reinterpret_cast<uint4 *>(ws.status + size_t(t) * 256)[tid] = make_uint4(0, 0, 0, 0);
-    if (known) continue;
+    if (known) {
+      // nothing to count: keys-only sorts skip to the bucket's last tile
+      if (!ws.stable) t = min(t1, bk.tile0 + uint32_t((bk.count + ws.tile - 1) / ws.tile)) - 1u;
+      continue;
+    }
     const uint64_t off = uint64_t(t - bk.tile0) * ws.tile;
     const uint32_t cnt = uint32_t(min64(ws.tile, bk.count - off));
     const K *src = static_cast<const K *>(ws.keys[bk.parity]) + bk.start + off;
