@@ -229,16 +229,15 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   constexpr bool WSPEC = VB == 0;  // keys-only: warp-specialised scatter
   auto sc = scatter_kernel<K, VB, KIND, SC_BLOCK, SKPT>;
   auto sw = scatter_ws_kernel<K, KIND, SC_BLOCK, SKPT, SC_NBUF>;
-  // dense local sort (bitmap enumeration): 512 consumers, 5632-key tasks,
-  // 2-slot ring; big variant (u32 only) 18432-key tasks (e.g. 2^30-key
-  // inputs), single slot
-  constexpr int DN_BLOCK = 512;
-  constexpr int D2_BLOCK = 256, DN_CAP = 4608, DN_SLOTS = 2;
-  constexpr int DB_CAP = sizeof(K) == 4 ? 18432 : 6144;
-  using DS = Dense2Smem<K, D2_BLOCK, DN_CAP, DN_SLOTS>;
-  using DB = DenseSmem<K, DN_BLOCK, DB_CAP, 1>;
-  auto dk = dense2_kernel<K, KIND, D2_BLOCK, DN_CAP, DN_SLOTS>;
-  auto db = dense_kernel<K, KIND, DN_BLOCK, DB_CAP, 1, true>;
+  // dense local sort (bitmap enumeration): small tasks 256 consumers, 4608
+  // keys, 2-slot ring (4 CTAs/SM); big variant (u32 only) 512 consumers,
+  // 18432-key tasks (e.g. 2^30-key inputs), one slot, 2 CTAs/SM
+  constexpr int DN_BLOCK = 256, DN_CAP = 4608, DN_SLOTS = 2;
+  constexpr int DB_BLOCK = 512, DB_CAP = sizeof(K) == 4 ? 18432 : 6144, DB_SLOTS = 1;
+  using DS = DenseSmem<K, DN_BLOCK, DN_CAP, DN_SLOTS, false>;
+  using DB = DenseSmem<K, DB_BLOCK, DB_CAP, DB_SLOTS, true>;
+  auto dk = dense_kernel<K, KIND, DN_BLOCK, DN_CAP, DN_SLOTS, false>;
+  auto db = dense_kernel<K, KIND, DB_BLOCK, DB_CAP, DB_SLOTS, true>;
   ws.dense_max = DN_CAP;
   ws.dense_big_max = sizeof(K) == 4 ? DB_CAP : 0;
   auto lc = local_kernel<K, VB, KIND, LC_BLOCK, LC_KPT>;
@@ -270,9 +269,9 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
                              : cudaSuccess;
     if (VB == 0 && e4 == cudaSuccess)
       e4 = cudaFuncSetAttribute(db, cudaFuncAttributeMaxDynamicSharedMemorySize, int(DB::bytes));
-    db_grid = VB == 0 ? num_sms() * max_active(db, DN_BLOCK + 32, DB::bytes) : 0;
+    db_grid = VB == 0 ? num_sms() * max_active(db, DB_BLOCK + 32, DB::bytes) : 0;
     attr_err = e1 != cudaSuccess ? e1 : (e2 != cudaSuccess ? e2 : (e3 != cudaSuccess ? e3 : e4));
-    dk_grid = VB == 0 ? num_sms() * max_active(dk, D2_BLOCK + 32, DS::bytes) : 0;
+    dk_grid = VB == 0 ? num_sms() * max_active(dk, DN_BLOCK + 32, DS::bytes) : 0;
     sc_grid = WSPEC ? num_sms() * max_active(sw, SC_BLOCK + 32, SW::bytes)
                     : num_sms() * max_active(sc, SC_BLOCK, SS::bytes);
     lc_grid = num_sms() * max_active(lc, LC_BLOCK, LS::bytes);
@@ -315,14 +314,14 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
       if constexpr (VB == 0) {
         // big dense children of this level (their data is in place now)
         if (ws.dense && ws.dense_big_max && L < nlev - 1)
-          BS_CUDA(pdl_launch(db, db_grid, DN_BLOCK + 32, DB::bytes, st, ws, L));
+          BS_CUDA(pdl_launch(db, db_grid, DB_BLOCK + 32, DB::bytes, st, ws, L));
       }
       BS_CUDA(pdl_launch(expand_kernel, num_sms() * 4, 256, 0, st, ws, L + 1));
       mark(st);
     }
   }
   if constexpr (VB == 0) {
-    if (ws.dense) BS_CUDA(pdl_launch(dk, dk_grid, D2_BLOCK + 32, DS::bytes, st, ws));
+    if (ws.dense) BS_CUDA(pdl_launch(dk, dk_grid, DN_BLOCK + 32, DS::bytes, st, ws, 0));
   }
   if constexpr (SPREAD) {
     BS_CUDA(pdl_launch(sp, sp_grid, SP_BLOCK, SPS::bytes, st, ws));
