@@ -89,7 +89,6 @@ static int num_sms() {
 struct Tune {
   int sc_block, sc_kpt, lc_block, lc_kpt;
 };
-constexpr int SC_NBUF = 2;
 //   8 B keys only: local 1024x8 (twice the warps per task for the latency-bound local bin sort)
 constexpr Tune tune_for(int kb, int vb) {
   return (kb + vb) <= 4   ? Tune{512, 16, 512, 16}
@@ -224,6 +223,9 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   constexpr int SC_BLOCK = TN.sc_block, SKPT = TN.sc_kpt, LC_BLOCK = TN.lc_block, LC_KPT = TN.lc_kpt;
   constexpr int HI_BLOCK = SC_BLOCK, HKPT = SKPT;  // histogram tiles == scatter tiles
   using SS = ScatterSmem<K, VB, KIND, SC_BLOCK, SKPT>;
+  // keys-only scatter ring: three tile slots for 4-byte keys (101 KB, still 2 CTAs/SM: 0.614 -> 0.605 ms
+  // per cfg2 pass), two for 8-byte keys (three CTAs/SM)
+  constexpr int SC_NBUF = sizeof(K) == 4 ? 3 : 2;
   using SW = ScatterWsSmem<K, KIND, SC_BLOCK, SKPT, SC_NBUF>;
   using LS = LocalSmem<K, VB, KIND, LC_BLOCK, LC_KPT>;
   constexpr bool WSPEC = VB == 0;  // keys-only: warp-specialised scatter
@@ -232,7 +234,7 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   // dense local sort (bitmap enumeration): small tasks 256 consumers, 4608
   // keys, 2-slot ring (4 CTAs/SM); big variant (u32 only) 512 consumers,
   // 18432-key tasks (e.g. 2^30-key inputs), one slot, 2 CTAs/SM
-  constexpr int DN_BLOCK = 256, DN_CAP = 4608, DN_SLOTS = 2;
+    constexpr int DN_BLOCK = 256, DN_CAP = 4608, DN_SLOTS = 2;
   constexpr int DB_BLOCK = 512, DB_CAP = sizeof(K) == 4 ? 18432 : 6144, DB_SLOTS = 1;
   using DS = DenseSmem<K, DN_BLOCK, DN_CAP, DN_SLOTS, false>;
   using DB = DenseSmem<K, DB_BLOCK, DB_CAP, DB_SLOTS, true>;
