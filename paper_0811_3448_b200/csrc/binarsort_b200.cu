@@ -245,8 +245,10 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   auto lc = local_kernel<K, VB, KIND, LC_BLOCK, LC_KPT>;
   // keys-only 64-bit: spread tasks go to spread_kernel first (1024 x 8 = local_max)
   constexpr bool SPREAD = VB == 0 && sizeof(K) == 8;
-  constexpr int SP_BLOCK = 1024, SP_KPT = 8;
-  static_assert(!SPREAD || SP_BLOCK * SP_KPT == LC_BLOCK * LC_KPT, "spread tasks are local tasks");
+  // 512 x 9 = 4608-key slots (~107 KB): two CTAs per SM, so one task's barriers hide behind the
+  // other's work; local tasks larger than a slot stay on local_kernel
+  constexpr int SP_BLOCK = 512, SP_KPT = 9;
+  static_assert(!SPREAD || SP_BLOCK * SP_KPT <= LC_BLOCK * LC_KPT, "spread tasks are local tasks");
   using SPS = SpreadSmem<K, SP_BLOCK, SP_KPT>;
   auto sp = spread_kernel<K, KIND, SP_BLOCK, SP_KPT>;
   auto hk = hist_kernel<K, KIND, HI_BLOCK, HKPT>;

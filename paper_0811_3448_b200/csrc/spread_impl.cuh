@@ -24,7 +24,7 @@ namespace bs {
 
 template <typename K, int BLOCK, int KPT>
 struct SpreadSmem {
-  static constexpr int CAP = BLOCK * KPT;                               // keys per task (== local_max)
+  static constexpr int CAP = BLOCK * KPT;                               // keys per task (<= local_max; larger ones: local_kernel)
   static constexpr size_t kbuf = (sizeof(K) * CAP + 32 + 15) & ~size_t(15);  // input slot, then staging
   static constexpr size_t buf_off = 0;                                  // two slots: the next task streams in
   static constexpr size_t bins_off = buf_off + 2 * kbuf;                // B1, B2, B3, P: 4 x 2048 words
@@ -42,7 +42,8 @@ __device__ __forceinline__ void push_task2(const Ws &ws, uint64_t start, uint32_
 }
 
 template <typename K, int KIND, int BLOCK, int KPT>
-__global__ void __launch_bounds__(BLOCK, 1) spread_kernel(Ws ws) {
+__global__ void __launch_bounds__(BLOCK, BLOCK <= 512 ? 2 : 1) spread_kernel(Ws ws) {
+  static_assert(BLOCK >= 512, "threads 0..511 own the bitmap words");
   pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
   if (ws_failed(ws)) return;
   using S = SpreadSmem<K, BLOCK, KPT>;
@@ -67,12 +68,18 @@ __global__ void __launch_bounds__(BLOCK, 1) spread_kernel(Ws ws) {
       f.cnt = tk.count;
       f.parity = tk.parity & 1u;
       f.digit = tk.parity >> 8;  // first digit that may vary: the prefix is it and the next one
-      const Span sk = span16(static_cast<const K *>(ws.keys[f.parity]) + f.start, f.cnt);
-      f.headk = sk.head;
-      info[sl] = f;
-      fence_proxy_async_smem();
-      mbar_arrive_expect_tx(&bars[sl], sk.bytes);
-      bulk_g2s(slot_keys(sl), sk.base, sk.bytes, &bars[sl]);
+      f.valid = tk.count <= uint32_t(S::CAP);  // larger local tasks go to local_kernel
+      if (f.valid) {
+        const Span sk = span16(static_cast<const K *>(ws.keys[f.parity]) + f.start, f.cnt);
+        f.headk = sk.head;
+        info[sl] = f;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&bars[sl], sk.bytes);
+        bulk_g2s(slot_keys(sl), sk.base, sk.bytes, &bars[sl]);
+      } else {
+        info[sl] = f;
+        mbar_arrive(&bars[sl]);
+      }
     } else {
       info[sl] = f;
     }
@@ -92,6 +99,10 @@ __global__ void __launch_bounds__(BLOCK, 1) spread_kernel(Ws ws) {
     phase ^= 1u << cur;
     K *kb = slot_keys(cur);
     const InFlight f = info[cur];
+    if (!f.valid) {  // more keys than a slot holds
+      if (tid == 0) push_task2(ws, f.start, f.cnt, f.parity);
+      continue;
+    }
     const int n = int(f.cnt);
     const int head = int(f.headk);
     // keys in registers: element tid + j*BLOCK (strided: conflict-free)
@@ -140,7 +151,7 @@ __global__ void __launch_bounds__(BLOCK, 1) spread_kernel(Ws ws) {
       if (tid == 0) push_task2(ws, f.start, f.cnt, f.parity);
       continue;
     }
-    // word offsets: thread t < 512 owns words 4t..4t+3; P[q] = keys before word q
+    // word offsets: thread t < 512 owns words 4t..4t+3 (BLOCK >= 512); P[q] = keys before word q
     // (| bit 31 when the word holds a repeated prefix)
     {
       const bool own = tid < 512;
