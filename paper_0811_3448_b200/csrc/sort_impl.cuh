@@ -1656,7 +1656,7 @@ struct LocalSmem {
 };
 
 template <typename K, int VB, int KIND, int BLOCK, int KPT>
-__global__ void __launch_bounds__(BLOCK) local_kernel(Ws ws, int list) {
+__global__ void __launch_bounds__(BLOCK, (VB == 0 && sizeof(K) == 8 && BLOCK <= 512) ? 2 : 1) local_kernel(Ws ws, int list) {
   pdl_wait();  // programmatic dependent launch: previous kernel's writes visible
   if (ws_failed(ws)) return;
   using S = LocalSmem<K, VB, KIND, BLOCK, KPT>;
