@@ -376,9 +376,13 @@ def run_gpu(args):
 
     from paper_0811_3448_b200.dist import SAMPLES_PER_RANK, dist_sort
 
+    exch = {"mode": "auto", "ran": "", "note": ""}  # N>1: which data exchange dist_sort uses
+
     def one_sort(phases=None, marks=None):
         if world > 1:
-            return dist_sort(work, width=32, marks=marks)
+            res = dist_sort(work, width=32, marks=marks, exchange=exch["mode"])
+            exch["ran"] = res.exchange
+            return res
         if phases is None:
             return device.sort_words_device(work, width=32, workspace=ws, check=False)
         buf = (ctypes.c_float * nev)()
@@ -410,32 +414,48 @@ def run_gpu(args):
             print("bench: GPU output differs from np.sort", file=sys.stderr)
             return 1
     else:
-        # this rank's slice sorted, slices in rank order, and the multiset kept:
-        # order-independent checksums of every input shard and every output slice
         import torch.distributed as dist
 
-        k = r.keys.to(torch.int64) & 0xFFFFFFFF
-        ok = bool((k[1:] >= k[:-1]).all()) if k.numel() > 1 else True
-        sums = torch.cat([_checksum(pristine), _checksum(r.keys)]).to("cpu" if share else dev)
-        dist.all_reduce(sums)
-        s = [int(v) for v in sums.cpu()]
-        ok = ok and s[0] == s[2] and s[1] == s[3]
-        ends = torch.tensor([k.numel(), int(k[0]) if k.numel() else -1, int(k[-1]) if k.numel() else -1,
-                             sum(r.send_counts) - r.send_counts[rank]],
-                            dtype=torch.int64, device="cpu" if share else dev)
-        allends = [torch.empty_like(ends) for _ in range(world)]
-        dist.all_gather(allends, ends)
-        e = [[int(v) for v in t.cpu()] for t in allends]
-        ok = ok and sum(x[0] for x in e) == total_keys
-        a2a_max = 4 * max(x[3] for x in e)  # bytes the busiest rank sends to other ranks
-        last = -1
-        for cnt, lo, hi, _ in e:
-            if cnt:
-                ok = ok and lo >= last
-                last = hi
-        flag = torch.tensor([1 if ok else 0], dtype=torch.int64, device="cpu" if share else dev)
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)  # every rank takes the same exit
-        if int(flag.item()) == 0:
+        def validate(r):
+            """This rank's slice sorted, slices in rank order, and the multiset kept (order-independent
+            checksums of every input shard and every output slice); the same verdict on every rank."""
+            k = r.keys.to(torch.int64) & 0xFFFFFFFF
+            ok = bool((k[1:] >= k[:-1]).all()) if k.numel() > 1 else True
+            sums = torch.cat([_checksum(pristine), _checksum(r.keys)]).to("cpu" if share else dev)
+            dist.all_reduce(sums)
+            s = [int(v) for v in sums.cpu()]
+            ok = ok and s[0] == s[2] and s[1] == s[3]
+            ends = torch.tensor([k.numel(), int(k[0]) if k.numel() else -1, int(k[-1]) if k.numel() else -1,
+                                 sum(r.send_counts) - r.send_counts[rank]],
+                                dtype=torch.int64, device="cpu" if share else dev)
+            allends = [torch.empty_like(ends) for _ in range(world)]
+            dist.all_gather(allends, ends)
+            e = [[int(v) for v in t.cpu()] for t in allends]
+            ok = ok and sum(x[0] for x in e) == total_keys
+            a2a = 4 * max(x[3] for x in e)  # bytes the busiest rank sends to other ranks
+            last = -1
+            for cnt, lo, hi, _ in e:
+                if cnt:
+                    ok = ok and lo >= last
+                    last = hi
+            flag = torch.tensor([1 if ok else 0], dtype=torch.int64, device="cpu" if share else dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)  # every rank takes the same exit
+            return int(flag.item()) == 1, a2a
+
+        ok, a2a_max = validate(r)
+        if not ok and exch["ran"] == "peer":
+            # the fused peer-store exchange gave a wrong result on this machine: fall back to the
+            # NCCL all-to-all exchange (every rank takes this branch: the verdict is all-reduced)
+            print(f"bench: rank {rank}: peer exchange failed validation; retrying with exchange='collective'",
+                  file=sys.stderr)
+            exch["mode"] = "collective"
+            exch["note"] = " (the peer-store exchange failed validation on this machine)"
+            for i in range(max(1, args.warmup)):
+                work.copy_(pristine)
+                r = one_sort()
+            torch.cuda.synchronize()
+            ok, a2a_max = validate(r)
+        if not ok:
             print(f"bench: rank {rank}: distributed output not globally sorted / multiset changed", file=sys.stderr)
             dist.destroy_process_group()
             return 1
@@ -497,7 +517,9 @@ def run_gpu(args):
         "data": f"synthetic ({'MT19937 seed 1+rank, cfg2 stream' if cfg == 'cfg2' else 'MT19937 seed 4, cfg5 stream'})",
         "config": {"workload": workload, "global_batch": total_keys, "keys_per_rank": n,
                    "parallelism": "single GPU" if world == 1 else
-                   f"range-partition x{world}: fused partition + NVLink peer stores (CUDA IPC), NCCL for counts",
+                   (f"range-partition x{world}: fused partition + NVLink peer stores (CUDA IPC), NCCL for counts"
+                    if exch["ran"] == "peer" else
+                    f"range-partition x{world}: partition + NCCL all-to-all-v" + exch["note"]),
                    "l2": f"inputs {4 * n / 2**20:.0f} MiB/rank > 126 MB L2; pristine copy restored between steps "
                          "(outside events)"},
         "clocks": clocks,
@@ -568,7 +590,7 @@ def run_gpu(args):
                                  "frac": (t_hbm + t_nvl) * 1e3 / ms,
                                  "def": "SURVEY 8d: 2*(N/R)*kb*P_alg/hbm_gbs + A2A_bytes_max_rank/900 GB/s"}
         if not args.no_e2e:
-            line["e2e"] = e2e_dist(args, host, dev, world, share, total_keys)
+            line["e2e"] = e2e_dist(args, host, dev, world, share, total_keys, exch["mode"])
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -578,7 +600,7 @@ def run_gpu(args):
     return 0
 
 
-def e2e_dist(args, host: np.ndarray, dev, world: int, share: bool, total_keys: int):
+def e2e_dist(args, host: np.ndarray, dev, world: int, share: bool, total_keys: int, exchange: str = "auto"):
     """N>1 end to end through the public multi-GPU API: every rank copies its
     shard from pinned host memory, runs dist_sort, and reads its slice of the
     global order back into pinned host memory; max over ranks."""
@@ -597,7 +619,7 @@ def e2e_dist(args, host: np.ndarray, dev, world: int, share: bool, total_keys: i
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         keys = pinned_src.to(dev, non_blocking=True)
-        r = dist_sort(keys, width=32)
+        r = dist_sort(keys, width=32, exchange=exchange)
         out = pinned_out[:r.keys.numel()] if r.keys.numel() <= pinned_out.numel() else \
             torch.empty(r.keys.numel(), dtype=r.keys.dtype).pin_memory()
         out.copy_(r.keys, non_blocking=True)

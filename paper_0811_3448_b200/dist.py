@@ -46,7 +46,7 @@ import numpy as np
 from . import _lib, device
 
 __all__ = ["CudaOps", "DistResult", "PeerBuffers", "choose_splitters", "boundaries", "send_counts",
-           "exchange_plan", "dist_sort"]
+           "exchange_plan", "dist_sort", "PeerUnavailable"]
 
 
 @dataclass
@@ -55,6 +55,7 @@ class DistResult:
     values: object | None
     send_counts: list[int]
     recv_counts: list[int]
+    exchange: str = ""  # the data exchange that ran: "peer", "collective" (or "" for one rank)
 
 
 class CudaOps:
@@ -165,6 +166,10 @@ class CudaOps:
         return out_k, out_v
 
 
+class PeerUnavailable(RuntimeError):
+    """The CUDA IPC peer mappings could not be set up (raised on EVERY rank of the group)."""
+
+
 class PeerBuffers:
     """Per-rank receive buffers mapped into every rank's address space (CUDA IPC).
 
@@ -202,26 +207,65 @@ class PeerBuffers:
         hb = int(L.bs_ipc_handle_bytes())
         handle = (ctypes.c_ubyte * hb)()
         ptr = ctypes.c_void_p()
-        with torch.cuda.device(self.device):
-            _lib.check(L.bs_ipc_alloc(nbytes, ctypes.byref(ptr), handle))
-        self._local = ptr.value
-        handles = _all_gather_np(np.frombuffer(bytes(handle), dtype=np.uint8), self.group, self.device)
+        # Every step that can fail on ONE rank (allocation, opening a peer's
+        # handle) is followed by an all-gathered verdict, so all ranks take the
+        # same exit: a rank that raised alone would leave the others waiting in
+        # the next collective.
+        why = ""
+        try:
+            with torch.cuda.device(self.device):
+                _lib.check(L.bs_ipc_alloc(nbytes, ctypes.byref(ptr), handle))
+            self._local = ptr.value
+        except Exception as e:  # noqa: BLE001 - reported collectively below
+            why = f"rank {me}: bs_ipc_alloc: {e}"
+        msg = np.zeros(hb + 1, dtype=np.uint8)
+        msg[:hb] = np.frombuffer(bytes(handle), dtype=np.uint8)
+        msg[hb] = 0 if why else 1
+        allmsg = _all_gather_np(msg, self.group, self.device)
+        handles = allmsg[:, :hb]
         bases = []
-        with torch.cuda.device(self.device):
-            for r in range(R):
-                if r == me:
-                    bases.append(self._local)
-                    continue
-                p = ctypes.c_void_p()
-                _lib.check(L.bs_ipc_open(handles[r].tobytes(), ctypes.byref(p)))
-                self._peers.append(p.value)
-                bases.append(p.value)
+        if allmsg[:, hb].all():
+            try:
+                with torch.cuda.device(self.device):
+                    for r in range(R):
+                        if r == me:
+                            bases.append(self._local)
+                            continue
+                        p = ctypes.c_void_p()
+                        _lib.check(L.bs_ipc_open(handles[r].tobytes(), ctypes.byref(p)))
+                        self._peers.append(p.value)
+                        bases.append(p.value)
+            except Exception as e:  # noqa: BLE001
+                why = f"rank {me}: bs_ipc_open: {e}"
+        elif not why:
+            why = "a peer could not allocate its receive buffer"
+        verdict = _all_gather_np(np.array([0 if why else 1], dtype=np.uint8), self.group, self.device)
+        if not verdict.all():
+            self._abort()
+            bad = [int(r) for r in np.nonzero(verdict[:, 0] == 0)[0]]
+            raise PeerUnavailable(why or f"peer mapping failed on rank(s) {bad}")
         self.key_table = torch.tensor(bases, dtype=torch.int64, device=self.device)
         self.val_table = torch.tensor([b + voff for b in bases], dtype=torch.int64, device=self.device)
         self.local_keys = self._local
         self.local_vals = self._local + voff
         self.cap, self.kb, self.vb = cap, kb, vb
         return self
+
+    def _abort(self) -> None:
+        """Collective clean-up after a failed ``ensure``: every rank runs both barriers."""
+        import torch
+
+        L = _lib.lib()
+        torch.cuda.synchronize(self.device)
+        _host_barrier(self.group, self.device)
+        for p in self._peers:
+            L.bs_ipc_close(p)
+        _host_barrier(self.group, self.device)
+        if self._local is not None:
+            L.bs_ipc_free(self._local)
+        self._local = None
+        self._peers = []
+        self.cap = 0
 
     def close(self) -> None:
         if self._local is None:
@@ -243,6 +287,7 @@ class PeerBuffers:
 
 
 _PEER_BUFFERS: dict = {}
+_NO_PEER: set = set()  # groups whose peer mappings failed once: exchange="auto" stays collective
 
 
 def _peer_buffers(group, dev) -> PeerBuffers:
@@ -442,11 +487,12 @@ def dist_sort(keys, values=None, *, width: int, key_kind: int = _lib.BS_KEY_UNSI
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     if R > MAX_RANKS:
         raise ValueError(f"dist_sort supports at most {MAX_RANKS} ranks (one NVSwitch node), got {R}")
+    auto = exchange == "auto"
     if exchange != "collective" and R > 1:
         cuda_path = isinstance(ops, CudaOps) and getattr(keys, "is_cuda", False)
         one_node = cuda_path and _single_node(group, R)
         if exchange == "auto":
-            exchange = "peer" if one_node else "collective"
+            exchange = "peer" if one_node and id(group) not in _NO_PEER else "collective"
         elif not one_node:
             raise ValueError("exchange='peer' needs CUDA tensors and every rank on one node (CUDA IPC)")
     if R == 1:
@@ -454,7 +500,20 @@ def dist_sort(keys, values=None, *, width: int, key_kind: int = _lib.BS_KEY_UNSI
         return DistResult(k, v, [keys.numel()], [keys.numel()])
     dev = keys.device
     if exchange == "peer":
-        return _dist_sort_peer(keys, values, ops, group, R, rank, samples_per_rank, marks)
+        try:
+            res = _dist_sort_peer(keys, values, ops, group, R, rank, samples_per_rank, marks)
+            res.exchange = "peer"
+            return res
+        except PeerUnavailable as e:
+            # raised on every rank (PeerBuffers.ensure agrees collectively), before any data moved
+            if not auto:
+                raise
+            import warnings
+
+            warnings.warn(f"dist_sort: peer-memory exchange unavailable ({e}); using the collective exchange")
+            _NO_PEER.add(id(group))
+            if marks is not None:
+                del marks[:]
     # 1. splitters from gathered samples
     smp = ops.sample(keys, samples_per_rank if keys.numel() else 0)
     cnt = torch.tensor([smp.numel()], dtype=torch.int64, device=dev)
@@ -487,7 +546,7 @@ def dist_sort(keys, values=None, *, width: int, key_kind: int = _lib.BS_KEY_UNSI
         dist.all_to_all_single(recv_v, send_v, rcounts, scounts, group=group)
     # 5. local (stable) sort; sources arrive in rank order
     recv_k, recv_v = ops.sort(recv_k, recv_v)
-    return DistResult(recv_k, recv_v, scounts, rcounts)
+    return DistResult(recv_k, recv_v, scounts, rcounts, "collective")
 
 
 def _all_gather_dev(t, group):

@@ -182,6 +182,59 @@ def test_two_processes_peer_exchange_one_gpu():
         assert np.array_equal(outv, allv[order])
 
 
+def _ipc_fail_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_0811_3448_b200 import _lib as lib_mod
+        from paper_0811_3448_b200.dist import PeerUnavailable, dist_sort
+
+        torch.cuda.set_device(0)
+        L = lib_mod.lib()
+        real_open = L.bs_ipc_open
+        if rank == 1:  # one rank cannot map its peer: every rank must learn it
+            L.bs_ipc_open = lambda *a: lib_mod.BS_ERR_CUDA
+        rng = np.random.default_rng(rank)
+        k = rng.integers(0, 2 ** 32, 1 << 18, dtype=np.uint64).astype(np.uint32)
+        raised = False
+        try:
+            dist_sort(torch.from_numpy(k.view(np.int32)).cuda(), width=32, exchange="peer")
+        except PeerUnavailable:
+            raised = True
+        L.bs_ipc_open = real_open  # the clean-up left both ranks able to try again
+        r = dist_sort(torch.from_numpy(k.view(np.int32)).cuda(), width=32, exchange="peer")
+        q.put((rank, raised, k, r.keys.cpu().numpy().view(np.uint32), r.exchange))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(400)
+def test_peer_mapping_failure_is_collective():
+    """A rank that cannot open a peer's IPC handle makes EVERY rank raise PeerUnavailable (no rank is
+    left waiting in a collective), and the buffers are cleaned up so that a later call works."""
+    import torch.multiprocessing as mp
+
+    _lib.lib()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_fail_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = sorted([q.get(timeout=300) for _ in range(2)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert all(g[1] for g in got), "PeerUnavailable must be raised on every rank"
+    assert all(g[4] == "peer" for g in got)
+    allk = np.concatenate([g[2] for g in got])
+    assert np.array_equal(np.concatenate([g[3] for g in got]), np.sort(allk))
+
+
 @pytest.mark.timeout(600)
 def test_bench_two_ranks_share_one_gpu():
     """bench.py's N>1 path (torchrun, dist_sort with the fused peer exchange,
