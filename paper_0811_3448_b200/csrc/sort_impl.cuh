@@ -615,6 +615,36 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
   const int tid = threadIdx.x;
   const int cur = L & 1;
   const uint32_t nb = min(ws.ctl->nbuckets[L], ws.maxb);
+  // Whole-input counting (keys only, full-width words): when every varying
+  // bit of the root lies in the hist16 digit pair, the sorted output is a
+  // function of the 65536-bin histogram alone (value v repeated count[v]
+  // times), so no key moves: hist16 becomes its exclusive prefix and
+  // gen16_kernel writes the output (one read pass + one write pass).  Every
+  // CTA evaluates the same condition and the CTAs share the 256 rows of the
+  // histogram: row base from the root's digit counts (the row sums), then a
+  // scan of the row in place.
+  if (L == 0 && nb == 1u && ws.dense && !ws.stable && ws.ctl->h16_bad == 0u) {
+    const Bucket bk = ws.buckets[0][0];
+    const K var = K(ws.bor[0][0] ^ ws.band[0][0]);
+    const int dig = int(bk.digit);
+    const int shA = W - 16 - 8 * dig;
+    if (var != 0 && (KeyTraits<K>::clz(var) >> 3) == dig && shA >= 0 && (var & ~(K(0xFFFF) << shA)) == 0) {
+      __shared__ uint32_t s_rowbase[256];
+      s_rowbase[tid] = scan256_excl<256>(ws.bhist[0][tid], s_scan);
+      __syncthreads();
+      for (uint32_t r = blockIdx.x; r < 256u; r += gridDim.x) {
+        uint32_t *row = ws.hist16 + size_t(r) * 256;
+        const uint32_t e = scan256_excl<256>(row[tid], s_scan);
+        row[tid] = s_rowbase[r] + e;
+      }
+      if (blockIdx.x == 0 && tid == 0) {
+        ws.buckets[0][0].action = ACT_GEN;
+        ws.ctl->gen_shift = uint32_t(shA);
+        ws.ctl->gen = 1u;
+      }
+      return;
+    }
+  }
   for (uint32_t b = blockIdx.x; b < nb; b += gridDim.x) {
     const Bucket bk = ws.buckets[cur][b];
     uint32_t *hist = ws.bhist[cur] + size_t(b) * 256;
@@ -651,39 +681,6 @@ __global__ void __launch_bounds__(256) plan_kernel(Ws ws, int L) {
           else if (dig + 1 < ws.ndig) push_bucket(ws, L, bk.start, bk.count, uint32_t(dig + 1), bk.parity);
           else if (bk.parity) emit_tasks(ws, bk.start, bk.count, 1);  // every digit constant: all equal
         }
-        continue;
-      }
-    }
-    // Whole-input counting (keys only, full-width words): when every varying
-    // bit of the root lies in the hist16 digit pair, the sorted output is a
-    // function of the 65536-bin histogram alone (value v repeated count[v]
-    // times), so no key moves: hist16 becomes its exclusive prefix and
-    // gen16_kernel writes the output (one read pass + one write pass).
-    if (L == 0 && b == 0 && ws.dense && !ws.stable && ws.ctl->h16_bad == 0u) {
-      const int shA = W - 16 - 8 * dig;
-      if ((var & ~(K(0xFFFF) << shA)) == 0) {
-        uint4 *h4 = reinterpret_cast<uint4 *>(ws.hist16) + tid * 64;  // thread t: bins 256t .. 256t+255
-        uint32_t sum = 0;
-        for (int q = 0; q < 64; ++q) {
-          const uint4 v = h4[q];
-          sum += v.x + v.y + v.z + v.w;
-        }
-        uint32_t run = scan256_excl<256>(sum, s_scan);
-        for (int q = 0; q < 64; ++q) {
-          const uint4 v = h4[q];
-          uint4 o;
-          o.x = run, run += v.x;
-          o.y = run, run += v.y;
-          o.z = run, run += v.z;
-          o.w = run, run += v.w;
-          h4[q] = o;
-        }
-        if (tid == 0) {
-          ws.buckets[cur][b].action = ACT_GEN;
-          ws.ctl->gen_shift = uint32_t(shA);
-          ws.ctl->gen = 1u;
-        }
-        __syncthreads();
         continue;
       }
     }
