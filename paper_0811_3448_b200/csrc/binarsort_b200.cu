@@ -741,7 +741,11 @@ int bs_split_exchange(const void *keys, const void *vals, uint64_t n, int key_by
     auto kern = split_exchange_kernel<K, VB, KIND>;
     const size_t smem = ExchangeSmem<K, VB>::bytes;
     BS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    kern<<<w.ntiles, SPLIT_BLOCK, smem, st>>>(static_cast<const K *>(keys), vals, n, shift0,
+    // persistent grid: the per-CTA setup (splitters, class table) is paid once per resident CTA
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, SPLIT_BLOCK, smem);
+    const unsigned grid = unsigned(min64(w.ntiles, uint64_t(num_sms()) * uint64_t(per_sm > 0 ? per_sm : 1)));
+    kern<<<grid, SPLIT_BLOCK, smem, st>>>(static_cast<const K *>(keys), vals, n, shift0,
                                               static_cast<const K *>(splitters), nsp, w.tile_hist,
                                               reinterpret_cast<const long long *>(delta),
                                               reinterpret_cast<const unsigned long long *>(bounds), nranks,

@@ -590,9 +590,10 @@ __global__ void __launch_bounds__(SPLIT_BLOCK, sizeof(K) + VB <= 4 ? 4 : sizeof(
   const int ncls = 2 * nsp + 1;
   __shared__ K s_spl[SPLIT_MAXSP + 1];
   __shared__ uint8_t s_tab[256];
+  // once per CTA (the grid is persistent: a CTA takes tiles blockIdx.x,
+  // blockIdx.x + gridDim.x, ...): splitters, class table, boundaries, tables
   load_splitters(s_spl, spl, nsp);
   const SplitClass<K> sc{s_spl, nsp};
-  for (int i = tid; i < NW * 16; i += SPLIT_BLOCK) (&wrun[0][0])[i] = 0;
   if (tid <= nranks) s_bnd[tid] = bounds[tid];
   if (tid < nranks) {
     s_dk[tid] = dst_keys[tid];
@@ -601,12 +602,15 @@ __global__ void __launch_bounds__(SPLIT_BLOCK, sizeof(K) + VB <= 4 ? 4 : sizeof(
   __syncthreads();
   build_split_lut(s_tab, sc);
   const SplitLUT<K> sr{s_tab, sc};
-  __syncthreads();
   const V *vals = static_cast<const V *>(vals_);
-  const uint64_t base = uint64_t(blockIdx.x) * SPLIT_TILE;
-  const int cnt = int(min64(SPLIT_TILE, n - base));
   const int wbase = w * 32 * SPLIT_KPT;
   const uint32_t lt = lanemask_lt();
+  const uint32_t ntiles = uint32_t((n + SPLIT_TILE - 1) / SPLIT_TILE);
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  for (int i = tid; i < NW * 16; i += SPLIT_BLOCK) (&wrun[0][0])[i] = 0;
+  __syncthreads();  // also: the previous tile's write-out has left the staging buffer; the table is built
+  const uint64_t base = uint64_t(tile) * SPLIT_TILE;
+  const int cnt = int(min64(SPLIT_TILE, n - base));
   K x[SPLIT_KPT];
   V v[SPLIT_KPT];
   uint32_t dr[SPLIT_KPT];  // class | rank-in-warp << 8
@@ -658,24 +662,29 @@ __global__ void __launch_bounds__(SPLIT_BLOCK, sizeof(K) + VB <= 4 ? 4 : sizeof(
     __syncwarp();
   }
   __syncthreads();
-  if (tid < 16) {  // per-warp exclusive prefixes per class, then tile class bases
+  if (w == 0) {  // warp 0, lane c < 16: per-warp exclusive prefixes of class c, then the tile's class bases
     uint32_t run = 0;
-    for (int i = 0; i < NW; ++i) {
-      const uint32_t c = wrun[i][tid];
-      wrun[i][tid] = run;
-      run += c;
+    if (lane < 16)
+      for (int i = 0; i < NW; ++i) {
+        const uint32_t c = wrun[i][lane];
+        wrun[i][lane] = run;
+        run += c;
+      }
+    uint32_t incl = run;  // inclusive scan over the 16 classes (lanes >= 16 hold 0)
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += y;
     }
-    tb[tid + 1] = run;
+    if (lane < 16) {
+      tb[lane + 1] = incl;
+      if (lane == 0) tb[0] = 0;
+      // shard class-major position -> global position
+      s_g[lane] = (long long)tile_off[size_t(tile) * 16 + lane] + (lane < ncls ? delta[lane] : 0) -
+                  (long long)(incl - run);
+    }
   }
   __syncthreads();
-  if (tid == 0) {
-    tb[0] = 0;
-    for (int c = 1; c <= 16; ++c) tb[c] += tb[c - 1];
-  }
-  __syncthreads();
-  if (tid < 16)  // shard class-major position -> global position
-    s_g[tid] = (long long)tile_off[size_t(blockIdx.x) * 16 + tid] + (tid < ncls ? delta[tid] : 0) -
-               (long long)tb[tid];
 #pragma unroll
   for (int j = 0; j < SPLIT_KPT; ++j) {
     const int e = wbase + 32 * j + lane;
@@ -695,27 +704,39 @@ __global__ void __launch_bounds__(SPLIT_BLOCK, sizeof(K) + VB <= 4 ? 4 : sizeof(
   __shared__ uint32_t seg_start[24];
   __shared__ long long seg_off[24];
   __shared__ uint32_t seg_dst[24];
-  if (tid == 0) {
-    int k = 0;
-    for (int c = 0; c < 16; ++c) {
-      const uint32_t a0 = tb[c], b0 = tb[c + 1];
-      for (uint32_t i = a0; i < b0;) {
-        const unsigned long long gpos = (unsigned long long)(s_g[c] + (long long)i);
-        int d = 0;
-        while (d + 1 < nranks && gpos >= s_bnd[d + 1]) ++d;
-        uint32_t iend = b0;
-        if (d + 1 < nranks) {
-          const unsigned long long lim = s_bnd[d + 1] - (unsigned long long)s_g[c];
-          if (lim < iend) iend = uint32_t(lim);
-        }
-        seg_start[k] = i;
-        seg_off[k] = s_g[c] - (long long)s_bnd[d];
-        seg_dst[k] = uint32_t(d);
-        ++k;
-        i = iend;
+  if (w == 0) {
+    // lane c < 16 cuts class c's run [tb[c], tb[c+1]) at the destination
+    // boundaries that fall inside it; a scan over the lanes places its
+    // segments in the list (class order == position order)
+    uint32_t a0 = 0, b0 = 0;
+    long long gc = 0;
+    int d0 = 0, nseg = 0;
+    if (lane < 16) {
+      a0 = tb[lane], b0 = tb[lane + 1], gc = s_g[lane];
+      if (b0 > a0) {
+        const unsigned long long gfirst = (unsigned long long)(gc + (long long)a0);
+        const unsigned long long glast = (unsigned long long)(gc + (long long)b0) - 1ull;
+        while (d0 + 1 < nranks && gfirst >= s_bnd[d0 + 1]) ++d0;
+        int d1 = d0;
+        while (d1 + 1 < nranks && glast >= s_bnd[d1 + 1]) ++d1;
+        nseg = d1 - d0 + 1;
       }
     }
-    seg_start[k] = uint32_t(cnt);  // sentinel
+    int incl = nseg;
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) {
+      const int y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int k = incl - nseg;
+    uint32_t i = a0;
+    for (int d = d0; d < d0 + nseg; ++d, ++k) {
+      seg_start[k] = i;
+      seg_off[k] = gc - (long long)s_bnd[d];
+      seg_dst[k] = uint32_t(d);
+      if (d + 1 < nranks) i = uint32_t(min64(uint64_t(b0), uint64_t(s_bnd[d + 1] - (unsigned long long)gc)));
+    }
+    if (lane == 15) seg_start[incl] = uint32_t(cnt);  // sentinel
   }
   __syncthreads();
   int si = 0;
@@ -737,6 +758,7 @@ __global__ void __launch_bounds__(SPLIT_BLOCK, sizeof(K) + VB <= 4 ? 4 : sizeof(
       if constexpr (VB != 0) s_dv[seg_dst[sj]][o] = vstage[i];
     }
   }
+  }  // tiles
   // The receivers are ordered after this grid by stream order on this GPU
   // plus a collective later in the stream.  Release chain, explicit: every
   // CTA's stores (cumulative through the barrier) are ordered by a GPU-scope
