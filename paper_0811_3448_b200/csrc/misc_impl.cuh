@@ -702,8 +702,9 @@ __global__ void __launch_bounds__(SPLIT_BLOCK, sizeof(K) + VB <= 4 ? 4 : sizeof(
   // with one destination and one offset.  One thread lists the segments,
   // then each warp stores 32 consecutive positions per step.
   __shared__ uint32_t seg_start[24];
-  __shared__ long long seg_off[24];
-  __shared__ uint32_t seg_dst[24];
+  __shared__ K *seg_kp[24];  // segment k: position i of the tile goes to seg_kp[k][i]
+  __shared__ V *seg_vp[24];
+  __shared__ int s_nseg;
   if (w == 0) {
     // lane c < 16 cuts class c's run [tb[c], tb[c+1]) at the destination
     // boundaries that fall inside it; a scan over the lanes places its
@@ -731,31 +732,31 @@ __global__ void __launch_bounds__(SPLIT_BLOCK, sizeof(K) + VB <= 4 ? 4 : sizeof(
     int k = incl - nseg;
     uint32_t i = a0;
     for (int d = d0; d < d0 + nseg; ++d, ++k) {
+      const long long off = gc - (long long)s_bnd[d];
       seg_start[k] = i;
-      seg_off[k] = gc - (long long)s_bnd[d];
-      seg_dst[k] = uint32_t(d);
+      seg_kp[k] = s_dk[d] + off;
+      if constexpr (VB != 0) seg_vp[k] = s_dv[d] + off;
       if (d + 1 < nranks) i = uint32_t(min64(uint64_t(b0), uint64_t(s_bnd[d + 1] - (unsigned long long)gc)));
     }
-    if (lane == 15) seg_start[incl] = uint32_t(cnt);  // sentinel
+    if (lane == 15) {
+      seg_start[incl] = uint32_t(cnt);  // sentinel
+      s_nseg = incl;
+    }
   }
   __syncthreads();
-  int si = 0;
-  for (int base_i = w * 32; base_i < cnt; base_i += SPLIT_BLOCK) {
-    while (seg_start[si + 1] <= uint32_t(base_i)) ++si;  // warp-uniform
-    const int i = base_i + lane;
-    if (seg_start[si + 1] >= uint32_t(min(base_i + 32, cnt))) {  // whole chunk in one segment (usual)
-      const long long off = seg_off[si];
-      const uint32_t dd = seg_dst[si];
-      if (i < cnt) {
-        s_dk[dd][i + off] = stage[i];
-        if constexpr (VB != 0) s_dv[dd][i + off] = vstage[i];
+  // segment by segment: consecutive threads store consecutive addresses of one destination
+  const int nseg_all = s_nseg;
+  for (int k = 0; k < nseg_all; ++k) {
+    const uint32_t e0 = seg_start[k + 1];
+    K *const pk = seg_kp[k];
+    if constexpr (VB != 0) {
+      V *const pv = seg_vp[k];
+      for (uint32_t i = seg_start[k] + uint32_t(tid); i < e0; i += SPLIT_BLOCK) {
+        pk[i] = stage[i];
+        pv[i] = vstage[i];
       }
-    } else if (i < cnt) {
-      int sj = si;
-      while (seg_start[sj + 1] <= uint32_t(i)) ++sj;  // the chunk crosses a segment end
-      const uint64_t o = uint64_t((long long)i + seg_off[sj]);
-      s_dk[seg_dst[sj]][o] = stage[i];
-      if constexpr (VB != 0) s_dv[seg_dst[sj]][o] = vstage[i];
+    } else {
+      for (uint32_t i = seg_start[k] + uint32_t(tid); i < e0; i += SPLIT_BLOCK) pk[i] = stage[i];
     }
   }
   }  // tiles
