@@ -82,7 +82,8 @@ static int num_sms() {
 
 // ----- tuning (per record width) --------------------------------------------
 // Scatter tiles and local-sort capacity by record bytes (key + value):
-//   4 B  (u32 keys):              tile 512x16 = 8192, local 512x16 = 8192
+//   4 B  (u32 keys):              tile 512x22 = 11264 (per-tile barriers, scan and digit atomics amortised over
+//                                 more keys, 176-byte runs; 23+ keys per thread spill), local 512x16 = 8192
 //   8-12 B (u64 keys, KV):         tile 256x16 = 4096 (KV: 256x14, 3 CTAs/SM), local 512x16 = 8192 (u64 keys only: 512x9 = 4608, 2 CTAs/SM)
 //   16 B (u64 keys + u64 values):  tile 256x16 = 4096, local 512x8  = 4096
 // (local capacity is bounded by two TMA input buffers in 227 KB of smem)
@@ -91,7 +92,7 @@ struct Tune {
 };
 //   8 B keys only: local 512x9, two CTAs per SM (one task's barriers hide behind the other's work: cfg3-zipf 6.95 -> 6.45 ms)
 constexpr Tune tune_for(int kb, int vb) {
-  return (kb + vb) <= 4   ? Tune{512, 16, 512, 16}
+  return (kb + vb) <= 4   ? Tune{512, 22, 512, 16}
          : vb == 0        ? Tune{256, 16, 512, 9}
          : (kb + vb) < 16 ? Tune{256, 14, 512, 16}
                           : Tune{256, 16, 512, 8};
@@ -223,9 +224,9 @@ static int run_sort(void *keys, void *vals, uint64_t n, int width_eff, void *wsp
   constexpr int SC_BLOCK = TN.sc_block, SKPT = TN.sc_kpt, LC_BLOCK = TN.lc_block, LC_KPT = TN.lc_kpt;
   constexpr int HI_BLOCK = SC_BLOCK, HKPT = SKPT;  // histogram tiles == scatter tiles
   using SS = ScatterSmem<K, VB, KIND, SC_BLOCK, SKPT>;
-  // keys-only scatter ring: three tile slots for 4-byte keys (101 KB, still 2 CTAs/SM: 0.614 -> 0.605 ms
-  // per cfg2 pass), two for 8-byte keys (three CTAs/SM)
-  constexpr int SC_NBUF = sizeof(K) == 4 ? 3 : 2;
+  // keys-only scatter ring: two tile slots (4-byte keys: 2 x 44 KB, 2 CTAs/SM; a third slot of 8192-key
+  // tiles measured 0.605 ms per cfg2 pass, two slots of 11264-key tiles 0.580 ms)
+  constexpr int SC_NBUF = 2;
   using SW = ScatterWsSmem<K, KIND, SC_BLOCK, SKPT, SC_NBUF>;
   using LS = LocalSmem<K, VB, KIND, LC_BLOCK, LC_KPT>;
   constexpr bool WSPEC = VB == 0;  // keys-only: warp-specialised scatter
