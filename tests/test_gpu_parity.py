@@ -158,6 +158,9 @@ DISTS = {
     # dense local-sort tasks with second/third/fourth+ copies (B2, B3, overflow list)
     "dense_dups_u32": lambda n: _top_low(6, n, 1 << 10, 1 << 12),
     "dense_dups_sparse_u32": lambda n: _top_low(7, n, 1 << 10, 1 << 13),
+    # ~4096-key dense tasks over 2^14 values: a few dozen third copies each (the small variant's
+    # overflow list, below its hand-over threshold)
+    "dense_list_u32": lambda n: _top_low(13, n, 1 << 10, 1 << 14),
     # ~16K-key tasks for the big dense variant, with a few repeats
     "big_dense_u32": lambda n: _top_low(8, n, 1 << 8, 1 << 16),
     # local bin sort: equal keys ranked inside a bin (each value 2 / 3 times) and
