@@ -53,6 +53,15 @@ big = words(np.uint32, 1 << 22, 11)
 d = dev(big)
 device.sort_words_device(d, width=32)
 check(d, np.sort(big), "u32 2^22 keys (two scatter levels)")
+# dense tasks of ~4096 keys with second / third copies and overflow-list entries, and ~16K-key big ones
+for ntop, nlow, what in ((1 << 10, 1 << 14, "small dense tasks, listed copies"), (1 << 10, 1 << 12, "small dense tasks, hand-over"),
+                         (1 << 8, 1 << 16, "big dense tasks")):
+    r = np.random.default_rng(ntop + nlow)
+    top = (r.integers(0, ntop, 1 << 22).astype(np.uint32) * np.uint32(40503)) & np.uint32(0xFFFF)
+    dd = (top << np.uint32(16)) | r.integers(0, nlow, 1 << 22).astype(np.uint32)
+    d = dev(dd)
+    device.sort_words_device(d, width=32)
+    check(d, np.sort(dd), "u32 " + what)
 y = words(np.uint32, n, 2, hi=300) * np.uint32(65537)
 d = dev(y)
 device.sort_words_device(d, width=32)
