@@ -38,8 +38,9 @@
 // three bitmaps, one slot (two CTAs per SM cover each other's copy waits),
 // launched per level right after scatter(L).
 // A task with more repeats than the overflow list holds is handed to the
-// general local sort (small) or to the next MSD level as an ordinary bucket
-// (big), so the kernel is exact for any input.
+// general local sort (if it fits one of its tasks) or to the next MSD level as
+// an ordinary bucket (big tasks beyond that), so the kernel is exact for any
+// input.
 #pragma once
 
 #include "sort_impl.cuh"
@@ -246,7 +247,9 @@ __global__ void __launch_bounds__(BLOCK + 32, BIG ? 2 : 4) dense_kernel(Ws ws, i
       // too many repeats: hand the task to the general local sort (small) or
       // to the next MSD level as an ordinary bucket (big)
       if (tid == 0) {
-        if (BIG) push_bucket(ws, L, f.start, f.cnt, (f.digit >> 20) & 0xFu, f.parity & 1u);
+        // (only ranges the local sort cannot take become buckets: the bucket
+        // and tile lists are sized for buckets of more than local_max keys)
+        if (BIG && f.cnt > ws.local_max) push_bucket(ws, L, f.start, f.cnt, (f.digit >> 20) & 0xFu, f.parity & 1u);
         else emit_tasks(ws, f.start, f.cnt, f.parity & 1u);
         mbar_arrive(&empty[s]);
       }

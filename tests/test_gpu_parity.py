@@ -161,6 +161,10 @@ DISTS = {
     # ~4096-key dense tasks over 2^14 values: a few dozen third copies each (the small variant's
     # overflow list, below its hand-over threshold)
     "dense_list_u32": lambda n: _top_low(13, n, 1 << 10, 1 << 14),
+    # ~6500-key big dense tasks with 4 distinct low halves each: the big variant's overflow list runs
+    # over and every task is handed to the general local sort (a bucket list sized for > 8192-key
+    # buckets must not receive them: found by tools/fuzz_gpu.py)
+    "big_dense_handover_u32": lambda n: _top_low(14, n, 640, 4),
     # ~16K-key tasks for the big dense variant, with a few repeats
     "big_dense_u32": lambda n: _top_low(8, n, 1 << 8, 1 << 16),
     # local bin sort: equal keys ranked inside a bin (each value 2 / 3 times) and
