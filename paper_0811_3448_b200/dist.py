@@ -124,13 +124,21 @@ class CudaOps:
             rc = L.bs_split_count(keys.data_ptr(), n, kb, self.width, self.key_kind, splitters.data_ptr(), nranks,
                                   counts.data_ptr(), ws.data_ptr(), ws.numel(), device.stream_ptr(keys.device))
         _lib.check(rc)
+        # the workspace now holds THIS shard's per-tile class offsets, which exchange() reads
+        self._counted = (keys.data_ptr(), n, splitters.data_ptr(), nranks)
         return counts
 
     def exchange(self, keys, values, splitters, nranks: int, delta: np.ndarray, bounds: np.ndarray, bufs):
-        """Store every element into its destination's receive buffer (bs_split_exchange)."""
+        """Store every element into its destination's receive buffer (bs_split_exchange).
+
+        Must follow ``split_count`` of the same shard with the same splitters on this object
+        (the kernel reads the tile offsets that pass left in the workspace)."""
         t = device.require_cuda()
         L = _lib.lib()
         dev = keys.device
+        if getattr(self, "_counted", None) != (keys.data_ptr(), keys.numel(), splitters.data_ptr(), nranks):
+            raise ValueError("exchange() must follow split_count() of the same shard and splitters on this CudaOps "
+                             "(one CudaOps per source rank)")
         d_delta = t.from_numpy(np.ascontiguousarray(delta, dtype=np.int64)).to(dev, non_blocking=True)
         d_bounds = t.from_numpy(np.ascontiguousarray(bounds, dtype=np.int64)).to(dev, non_blocking=True)
         ws = self._split_ws
