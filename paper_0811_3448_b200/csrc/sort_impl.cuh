@@ -377,9 +377,17 @@ __global__ void __launch_bounds__(BLOCK, 1) hist16_kernel(Ws ws) {
   // 7 batches, so spread keys pay ~nothing for it.  The epoch bound is
   // unchanged (the same keys are counted).
   int skip = 0;  // batches until the next same-bin check (warp-uniform)
-  for (uint64_t eb = g0; eb < g1; eb += uint64_t(GPE) * BLOCK) {  // block-uniform epochs
-#pragma unroll
-    for (int u0 = 0; u0 < GPE; u0 += UNR) {
+  // Batches in the coming epoch (block-uniform): two in general (halves are
+  // below 0x8000 after a sweep, an epoch of 2 x 16384 keys adds at most
+  // 0x8000); three when the sweep saw every half below 0x4000 (3 x 16384 =
+  // 0xC000 more still fits 16 bits) -- the usual case for spread keys, and a
+  // third fewer barriers and sweeps.
+  static_assert(UNR * BLOCK * EPG <= 16384, "three batches add at most 0xC000 to a half");
+  int nbatch = GPE / UNR + 1;  // the bins start at zero
+  for (uint64_t eb = g0; eb < g1;) {  // block-uniform epochs
+    const int ebatch = nbatch;  // this epoch's batches (nbatch becomes the next epoch's below)
+#pragma unroll 1
+    for (int u0 = 0; u0 < ebatch * UNR; u0 += UNR) {
       uint4 v[UNR];
       K nk[UNR * EPG];
       uint32_t valid = 0;
@@ -467,8 +475,10 @@ __global__ void __launch_bounds__(BLOCK, 1) hist16_kernel(Ws ws) {
       }
     }
     __syncthreads();
+    uint32_t seen = 0;  // OR of this thread's words after the sweep
     for (int q = tid; q < 32768 / 4; q += BLOCK) {  // sweep (rarely finds anything)
       uint4 wv = reinterpret_cast<const uint4 *>(hw)[q];
+      seen |= (wv.x | wv.y | wv.z | wv.w) & 0x7FFF7FFFu;
       if ((wv.x | wv.y | wv.z | wv.w) & 0x80008000u) {
         uint32_t *ww = &wv.x;
 #pragma unroll
@@ -485,7 +495,9 @@ __global__ void __launch_bounds__(BLOCK, 1) hist16_kernel(Ws ws) {
         reinterpret_cast<uint4 *>(hw)[q] = wv;
       }
     }
-    __syncthreads();
+    // (the barrier the sweep needs anyway carries the verdict)
+    nbatch = __syncthreads_or((seen & 0x40004000u) != 0u) ? GPE / UNR : GPE / UNR + 1;
+    eb += uint64_t(ebatch) * UNR * BLOCK;
   }
   __syncthreads();
   // flush: this CTA's packed bins to its partial row (plain coalesced stores;
